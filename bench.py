@@ -1,0 +1,378 @@
+#!/usr/bin/env python3
+"""bench.py -- TGV explicit-FD RK time step on B200 (one JSON line on rank 0).
+
+Metric (BASELINE.json): grid-point updates per second per RK step, TGV,
+per precision mode; one step = one full low-storage RK3 step (3 substeps of
+residual + stage update + halo refresh).  Inputs are the deterministic TGV
+initial condition (synthetic, no RNG); the state (>= 5.4 GB at 512^3 DP) is
+far larger than the 126 MB L2, so no explicit flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 512] [--precision DP]
+  python bench.py --impl reference ...     # the reference CPU implementation
+
+Multi-GPU: launched by torch.distributed.run, one rank per GPU; z-slab
+decomposition of the n^3 cube with NCCL halo exchange (strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("grid-pt updates/s per RK step (TGV 512^3, per precision mode) at 1/2/4/8 B200; "
+          "% HBM roofline")
+UNIT = "grid-pt updates/s"
+BYTES = {"B16": 2, "B32": 4, "B64": 8}
+PRESET_KINDS = {  # (q, rk, res, wk) byte widths, precision.cpp:58-88
+    "DP": (8, 8, 8, 8), "SP": (4, 4, 4, 4), "HP": (2, 2, 2, 2), "SPDP": (8, 8, 4, 4),
+    "SPDP-wk": (8, 8, 8, 4), "SPDP-res": (8, 8, 4, 8), "HPSP": (4, 4, 2, 2),
+    "HPSP-wk": (4, 4, 4, 2), "HPSP-res": (4, 4, 2, 4),
+}
+DT = {64: 0.002, 128: 0.001, 256: 5e-4, 512: 2.5e-4, 1024: 1.25e-4}
+
+
+def b_alg(preset: str) -> int:
+    """B_alg = 45 bq + 30 br + 25 bt bytes / point / RK step."""
+    bq, bt, br, _ = PRESET_KINDS[preset]
+    return 45 * bq + 30 * br + 25 * bt
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_run(preset, strategy, emulation, steps, warmup, threads=None, n=None,
+                      budget_s=20.0):
+    """Time the reference CPU implementation (oracle/_ref, else the C port) on
+    this host on a bounded sample grid; returns (pt/s, cores, kind, sample)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+
+    threads = threads or os.cpu_count() or 1
+    kind = "reference" if po.ref_available() else "port"
+    # sample size: the per-point rate is grid-size independent on CPU; pick
+    # the largest of 48..128 whose step fits the budget (HPSP Strict ~8x DP)
+    slow = 8.0 if (emulation == "strict" and PRESET_KINDS[preset][2] == 2) else 1.0
+    est_rate = 2.0e6 * max(1, threads) / 8.0 / slow  # pt/s, SURVEY 6 (8 threads: ~2 Mpt/s DP)
+    if n is None:
+        n = 48
+        for cand in (64, 80, 96, 128):
+            if cand ** 3 / est_rate * (steps + warmup) <= budget_s:
+                n = cand
+    kw = dict(preset=preset, strategy=strategy, emulation=emulation)
+    if kind == "reference":
+        c = po.Reference(n, threads=threads, **kw)
+    else:
+        po.oracle_lib().orc_set_threads(threads)
+        c = po.Oracle(n, **kw)
+    c.init()
+    dt = DT.get(n, 0.002)
+    if warmup:
+        c.advance(dt, warmup, 0, threads=threads)
+    t0 = time.perf_counter()
+    c.advance(dt, steps, 0, threads=threads)
+    el = time.perf_counter() - t0
+    rate = n ** 3 * steps / el
+    sample = (f"TGV {n}^3 {preset} {strategy} {emulation}, {steps} RK steps after {warmup} "
+              f"warm-up, {'reference advance() (oracle/_ref)' if kind == 'reference' else 'C port (oracle/)'}, "
+              f"threads={threads}")
+    return rate, threads, kind, sample
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    rate, cores, kind, sample = cpu_reference_run(args.precision, args.strategy, args.emulation,
+                                                  args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": dtype_of(args.precision), "data": "synthetic",
+        "config": {"workload": f"TGV {args.n}^3 {args.precision}", "sample": sample},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def dtype_of(preset):
+    q, t, r, w = PRESET_KINDS[preset]
+    names = {8: "f64", 4: "f32", 2: "f16"}
+    return names[r] if q == r else f"{names[q]}/{names[r]}"
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--precision", default="DP")
+    ap.add_argument("--strategy", default="storesome")
+    ap.add_argument("--emulation", default="strict")
+    ap.add_argument("--split", default="Blaisdell")
+    ap.add_argument("--path", default="auto", choices=["auto", "fused", "staged"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--modes", default="SPDP,HPSP",
+                    help="extra precision modes measured after the headline (per_precision)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_20911_b200 as m
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    hbm, peak_src = peaks()
+
+    def measure(preset, with_extras):
+        n = args.n
+        dt = DT.get(n, 2.5e-4)
+        prec = m.resolve_preset(preset, args.emulation)
+        decomp = None
+        if world > 1:
+            obj = [m.Solver.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            decomp = m.Decomposition(pz=world, mode=1, rank=rank, device=local, nccl_id=obj[0])
+        else:
+            decomp = m.Decomposition(device=local)
+        s = m.Solver(m.GridSpec(n), prec, args.strategy, m.FlowParams(0.1, 1600.0, 0.72, 1.4, True),
+                     args.split, decomp)
+        if args.path != "auto":
+            s.set_path(args.path)
+        s.init_tgv()
+        s.run_steps(args.warmup, dt)
+        s.synchronize()
+        stream = torch.cuda.ExternalStream(s.stream)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.profile(True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            ev0.record(stream)
+            s.run_steps(args.steps, dt)
+            ev1.record(stream)
+            s.synchronize()
+            torch.cuda.synchronize()
+        ms_total = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ms_total], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_total = float(t.item())
+        kms, klaunch = s.profile_read()
+        s.profile(False)
+        ms_step = ms_total / args.steps
+        rate = n ** 3 / (ms_step * 1e-3)
+        # roofline of the dominant kernel (class 0: residual / fused step)
+        bq, bt, br, bw = PRESET_KINDS[preset]
+        nloc = n ** 3 // world
+        fused = klaunch[1] == 0
+        if fused:
+            # compulsory per substep: read Q, write Q; Qt read (substeps 1,2) + write
+            per_pt = (10 * bq + 5 * bt) / 3 + 2 * (10 * bq + 10 * bt) / 3
+            kname = "fused residual + RK stage update"
+        else:
+            per_pt = 5 * bq + 5 * br
+            kname = "staged residual (k_resid)"
+        avg_ms = kms[0] / max(1, klaunch[0])
+        achieved = per_pt * nloc / (avg_ms * 1e-3) / 1e9
+        res = {
+            "preset": preset, "value": rate, "ms_per_step": ms_step,
+            "b_alg_bytes_per_pt": b_alg(preset),
+            "b_alg_frac": rate * b_alg(preset) / 1e9 / hbm,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic_lookup(preset, n, fused),
+                         "kernel": kname, "avg_launch_ms": avg_ms,
+                         "bytes_per_pt_per_launch": per_pt, "peak_source": peak_src},
+            "kernel_ms": {"dominant": kms[0], "rk": kms[1], "halo": kms[2], "other": kms[3]},
+            "gpu_launches": int(klaunch[0] + klaunch[1] + klaunch[3]),
+            "clocks": clk.summary(),
+            "path": "fused" if fused else "staged",
+        }
+        if with_extras and not args.no_e2e:
+            res["e2e"] = e2e_run(m, s, n, dt, args.steps, world, rank)
+        dev, census, census64 = s.memory()
+        res["device_bytes"] = dev
+        s.close()
+        del s
+        torch.cuda.synchronize()
+        return res
+
+    head = measure(args.precision, True)
+    extra = {}
+    for p in [x for x in args.modes.split(",") if x and x != args.precision]:
+        try:
+            r = measure(p, False)
+            extra[p] = {k: r[k] for k in ("value", "ms_per_step", "b_alg_frac", "path")}
+            extra[p]["roofline_frac"] = r["roofline"]["frac"]
+        except Exception as e:  # report, never hide
+            extra[p] = {"error": str(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": dtype_of(args.precision), "data": "synthetic",
+            "config": {"workload": f"TGV {args.n}^3 {args.precision} (M=0.1, Re=1600, "
+                                   f"{args.split}, {args.strategy}, {args.emulation})",
+                       "n": args.n, "precision": args.precision, "path": head["path"],
+                       "decomposition": f"z-slabs x{world}",
+                       "l2": "state >> 126 MB L2 (no flush needed)"},
+            "roofline": head["roofline"],
+            "b_alg": {"bytes_per_pt_per_step": head["b_alg_bytes_per_pt"],
+                      "frac_of_hbm": head["b_alg_frac"]},
+            "gpu_launches": head["gpu_launches"],
+            "clocks": head["clocks"],
+            "kernel_ms": head["kernel_ms"],
+            "per_precision": {args.precision: {"value": head["value"],
+                                               "ms_per_step": head["ms_per_step"],
+                                               "b_alg_frac": head["b_alg_frac"]}, **extra},
+        }
+        if "e2e" in head:
+            line["e2e"] = head["e2e"]
+        if not args.no_cpu_baseline and world == 1:
+            try:
+                rate, cores, kind, sample = cpu_reference_run(args.precision, args.strategy,
+                                                              args.emulation, 2, 1)
+                line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores,
+                                        "kind": kind, "sample": sample}
+            except Exception as e:
+                line["cpu_baseline"] = {"value": None, "error": str(e)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def traffic_lookup(preset, n, fused):
+    """dram bytes per launch from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(f"{preset}/{n}/{'fused' if fused else 'staged'}")
+    except Exception:
+        return None
+
+
+def e2e_run(m, s_unused, n, dt, steps, world, rank):
+    """Same metric through the reference-facing C-ABI with HOST buffers:
+    pinned ext^3 binary64 carriers (the reference Field layout) uploaded,
+    `steps` RK steps advanced with a diagnostics sample (D2H) at the end,
+    the state read back; all inside the timed region."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    if world > 1:
+        return None
+    e = n + 8
+    # pinned host carriers for the 5 components of Q
+    host = [torch.empty((e, e, e), dtype=torch.float64, pin_memory=True) for _ in range(5)]
+    s = s_unused
+    s.init_tgv()
+    for c in range(5):
+        m.solver._check(s.L.mpfd_b200_get_state(
+            s.h, 0, c, C.cast(host[c].data_ptr(), C.POINTER(C.c_double))))
+    s.synchronize()
+    t0 = time.perf_counter()
+    for c in range(5):
+        m.solver._check(s.L.mpfd_b200_set_state(
+            s.h, 0, c, C.cast(host[c].data_ptr(), C.POINTER(C.c_double))))
+    r = s.advance(m.StepConfig(dt, steps, steps))
+    for c in range(5):
+        m.solver._check(s.L.mpfd_b200_get_state(
+            s.h, 0, c, C.cast(host[c].data_ptr(), C.POINTER(C.c_double))))
+    el = time.perf_counter() - t0
+    h2d = 5 * n ** 3 * 8 / steps
+    d2h = (5 * n ** 3 * 8 + 2 * 2 * (n ** 3 // 4096) * 8) / steps
+    return {"value": n ** 3 * steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h,
+            "note": "advance() through the C-ABI: Q uploaded from pinned ext^3 binary64 host "
+                    "carriers, diagnostics sampled at t=0 and t_end, Q read back; bytes "
+                    "amortised over the steps", "diverged": r.diverged}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,190 @@
+/* mpfd_b200.h -- C-ABI of the B200-native TGV explicit-FD RK time step.
+ *
+ * Drop-in boundary for the reference solver's hot path (mpfd,
+ * /root/reference/proj).  Every entry point names the reference interface it
+ * replaces; SURVEY.md section 8(b) is the contract.  Plain pointers and sizes
+ * only: no C++ exceptions, no torch types cross this ABI.
+ *
+ * Return codes (all int-returning calls):
+ *   MPFD_OK 0, MPFD_ECONFIG 1 (ConfigError/RegistryError in the reference,
+ *   precision.hpp:23-28), MPFD_DIVERGED 2 (RunStatus::Diverged,
+ *   integrate.hpp:35-43), MPFD_EDEVICE 3 (CUDA or NCCL failure).
+ * mpfd_b200_last_error() returns a thread-local message for the last failure.
+ *
+ * Ownership: the solver owns all device memory; the caller owns host
+ * buffers.  All calls on one solver come from one host thread (the
+ * reference's "one control thread" model).
+ */
+#ifndef MPFD_B200_H
+#define MPFD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPFD_OK 0
+#define MPFD_ECONFIG 1
+#define MPFD_DIVERGED 2
+#define MPFD_EDEVICE 3
+
+/* PrecisionKind (precision.hpp:31), numerically identical */
+enum { MPFD_B16 = 0, MPFD_B32 = 1, MPFD_B64 = 2 };
+/* EmulationMode (precision.hpp:54) */
+enum { MPFD_STRICT = 0, MPFD_STOREROUND = 1 };
+/* ResidualStrategy (physics.hpp:65-68) */
+enum { MPFD_DEFAULT = 0, MPFD_STORESOME = 1 };
+/* ArrayClass (precision.hpp:60-66) as used by set_state/get_state */
+enum { MPFD_Q_VECTOR = 0, MPFD_RK_ARRAYS = 1, MPFD_RESIDUALS = 2, MPFD_WK_ARRAYS = 3 };
+/* KeWeighting (tgv.hpp:24-27) */
+enum { MPFD_KE_PLAIN = 0, MPFD_KE_DENSITY = 1 };
+/* decomposition transport */
+enum { MPFD_DECOMP_LOCAL = 0, MPFD_DECOMP_NCCL = 1 };
+
+/* GridSpec (field.hpp:20-56): cube n^3, spacing domain_length/n, halo 4. */
+typedef struct {
+    int n;
+    double domain_length; /* 0 -> 2*pi */
+} mpfd_grid;
+
+/* PrecisionConfig (precision.hpp:181-193) with custom_overrides as parallel
+ * arrays of (field name, PrecisionKind). */
+typedef struct {
+    int q_vector, rk_arrays, residuals, wk_arrays;
+    int emulation;
+    int n_overrides;
+    const char* const* override_names;
+    const int* override_kinds;
+} mpfd_precision;
+
+/* FlowParams (physics.hpp:26-34) */
+typedef struct {
+    double mach, reynolds, prandtl, gamma;
+    int viscous;
+} mpfd_flow;
+
+/* SplitCoefficients (physics.hpp:40-59) */
+typedef struct {
+    double alpha, beta_rho, beta_u, beta_phi, gamma_rho, gamma_u, gamma_phi;
+} mpfd_split;
+
+/* z-slab decomposition.  LOCAL: this process owns all pz slabs (one device
+ * or `devices[pz]`), halos move by device copies.  NCCL: one slab per
+ * process, `rank` of `pz`, communicator built from the 128-byte
+ * ncclUniqueId in `nccl_id` (see mpfd_b200_nccl_unique_id). */
+typedef struct {
+    int pz;
+    int mode;
+    int rank;
+    int device;
+    const int* devices; /* LOCAL only; NULL -> all slabs on `device` */
+    const void* nccl_id;
+} mpfd_decomp;
+
+/* DivergenceEvent (physics.hpp:85-91); code 1 "nonpositive or nonfinite
+ * density", 2 "nonfinite residual", 3 "nonfinite state" */
+typedef struct {
+    int code;
+    int i, j, k;
+    double time;
+    long iteration;
+    int substep;
+} mpfd_divergence;
+
+/* DiagnosticsRecord (tgv.hpp:13-20) */
+typedef struct {
+    double t, kinetic_energy, enstrophy, eps_s, ke_normalized;
+    int diverged;
+} mpfd_diag;
+
+/* RKScheme (integrate.hpp:18-22) + StepConfig (integrate.hpp:24-28) */
+typedef struct {
+    double a[3], b[3];
+    double dt;
+    long n_iterations;
+    int diagnostics_interval;
+    int ke_weighting;
+    int threads; /* reduction-tree shape of the reference's deterministic_sum
+                    (reduce.cpp:24-36): 1 = pure pairwise, >1 = 4096-chunked */
+} mpfd_step;
+
+typedef struct mpfd_solver mpfd_solver;
+
+const char* mpfd_b200_last_error(void);
+const char* mpfd_b200_version(void);
+
+/* resolve_preset (precision.cpp:58-88); emulation left Strict */
+int mpfd_b200_resolve_preset(const char* name, mpfd_precision* out);
+/* split_preset (physics.cpp:19-43) */
+int mpfd_b200_split_preset(const char* name, mpfd_split* out);
+/* 128-byte ncclUniqueId for MPFD_DECOMP_NCCL (rank 0 creates, broadcasts) */
+int mpfd_b200_nccl_unique_id(void* out128);
+
+/* make_solver_fields (physics.cpp:441-475) + ResidualEvaluator constructor
+ * (physics.cpp:477-483): allocates Q, Qt, R in HBM at their storage
+ * precisions.  strategy: MPFD_DEFAULT / MPFD_STORESOME. */
+int mpfd_b200_create(const mpfd_grid* grid, const mpfd_precision* prec, int strategy,
+                     const mpfd_flow* flow, const mpfd_split* split, const mpfd_decomp* decomp,
+                     mpfd_solver** out);
+int mpfd_b200_destroy(mpfd_solver* s);
+
+/* init_tgv / init_uniform (tgv.cpp:29-74): evaluated on the host in binary64
+ * (glibc sin/cos, bitwise the reference's), rounded, uploaded; Qt, R zeroed;
+ * Q halos refreshed. */
+int mpfd_b200_init_tgv(mpfd_solver* s);
+int mpfd_b200_init_uniform(mpfd_solver* s);
+
+/* Field carriers in the reference layout (field.hpp:45-51): ext^3 binary64,
+ * ext = n + 8, x fastest, interior at offset 4.  set rounds to the storage
+ * precision like Field::set (field.hpp:77-80); get widens exactly.  cls is
+ * MPFD_Q_VECTOR / MPFD_RK_ARRAYS / MPFD_RESIDUALS; comp 0..4.  Only the
+ * interior is read on set; get fills halos periodically. */
+int mpfd_b200_set_state(mpfd_solver* s, int cls, int comp, const double* ext3);
+int mpfd_b200_get_state(mpfd_solver* s, int cls, int comp, double* ext3);
+/* Same, interior-only n^3 carriers. */
+int mpfd_b200_set_state_interior(mpfd_solver* s, int cls, int comp, const double* n3);
+int mpfd_b200_get_state_interior(mpfd_solver* s, int cls, int comp, double* n3);
+
+/* ResidualEvaluator::evaluate (physics.cpp:485-587): R from Q (Q halos must
+ * be fresh).  Returns MPFD_DIVERGED with *ev filled on a density or
+ * nonfinite-residual signal. */
+int mpfd_b200_residual(mpfd_solver* s, mpfd_divergence* ev);
+/* rk_substep (integrate.cpp:47-91) with the caller's scheme coefficients.
+ * Returns MPFD_DIVERGED if the updated Q is nonfinite (the finite guard of
+ * advance, integrate.cpp:135-147). */
+int mpfd_b200_rk_substep(mpfd_solver* s, int substep, const double a[3], const double b[3],
+                         double dt, mpfd_divergence* ev);
+/* fill_state_halos (integrate.cpp:93-95) + the NCCL z-halo exchange. */
+int mpfd_b200_halo_refresh(mpfd_solver* s);
+/* DiagnosticsComputer::compute (tgv.cpp:115-175) */
+int mpfd_b200_diagnostics(mpfd_solver* s, int weighting, double t, int threads, mpfd_diag* out);
+/* advance (integrate.cpp:97-167): samples at t = 0, every
+ * diagnostics_interval iterations, and at divergence into series[cap].
+ * Returns MPFD_OK or MPFD_DIVERGED (*ev filled). */
+int mpfd_b200_advance(mpfd_solver* s, const mpfd_step* step, mpfd_diag* series, long cap,
+                      long* len, mpfd_divergence* ev, long* iters);
+
+/* --- measurement hooks (bench.py) --------------------------------------- */
+/* The solver's CUDA stream (cudaStream_t) for external event timing. */
+void* mpfd_b200_stream(mpfd_solver* s);
+int mpfd_b200_synchronize(mpfd_solver* s);
+/* Run `iters` RK steps with no sampling and no host sync; launches counted. */
+int mpfd_b200_run_steps(mpfd_solver* s, const mpfd_step* step, long iters);
+/* Per-kernel-class CUDA-event timing inside run_steps: enable, then read
+ * total ms and launch counts for classes 0 residual, 1 rk update,
+ * 2 halo, 3 other. */
+int mpfd_b200_profile(mpfd_solver* s, int enable);
+int mpfd_b200_profile_read(mpfd_solver* s, double ms[4], long launches[4]);
+/* Device memory held by the solver (bytes) and the analytic census of the
+ * reference's field set (memory_report, registry.cpp:24-39). */
+int mpfd_b200_memory(mpfd_solver* s, size_t* device_bytes, size_t* census_bytes,
+                     size_t* census_b64_bytes);
+/* Which residual path runs: 0 = staged multi-kernel, 1 = fused. */
+int mpfd_b200_set_path(mpfd_solver* s, int path);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,348 @@
+// kernels_staged.cuh -- the staged residual path (one kernel per level).
+//
+//   k_prim   primitives_impl        physics.cpp:281-331 (all Q planes, incl. ghosts)
+//   k_level2 divu / sum u tau / dT   physics.cpp:217-271 (+ ddx1 staging for
+//                                    the Default strategy, stencil.cpp:11-28)
+//   k_resid  residual_slab          physics.cpp:345-394 + finite scan :573-584
+//   k_rk     rk_substep             integrate.cpp:47-91 + Q finite guard :135-147
+//   k_diag_* DiagnosticsComputer    tgv.cpp:83-175 + deterministic_sum reduce.cpp:24-36
+//
+// HBM layout of one z-slab (nzl local planes, H = 4 ghost planes per side,
+// x/y periodic by index wrap, x fastest):
+//   Q    [nzl+2H planes][5 comp][ny][nx]   (comp-interleaved per plane: the
+//         4 boundary planes of all 5 components are one contiguous block, so
+//         a z-halo is one copy / one NCCL message)
+//   Qt,R [nzl][5][ny][nx]
+//   prim [5 field][nzl+2H][ny][nx]   (staged path only)
+//   lev2 [7 field][nzl+2H][ny][nx]   (staged path only)
+#pragma once
+
+#include "stencil.cuh"
+
+namespace mpfd_b200 {
+
+constexpr int kHalo = 4;
+
+struct Geo {
+    int nx, ny, nzl;  // local interior extents
+    int z0;           // global z of local plane 0
+    long long plane;  // nx*ny
+    int planes;       // nzl + 2*kHalo
+};
+
+// divergence record, first-in-scan-order per (code, component) via atomicMin
+struct DevDiv {
+    int flag;
+    int iter;
+    int sub;
+    int pad;
+    unsigned long long idx[3][5];
+};
+
+__device__ __forceinline__ void record_div(DevDiv* d, int code, int comp, unsigned long long gidx,
+                                           int iter, int sub) {
+    atomicMin(&d->idx[code][comp], gidx);
+    d->iter = iter;
+    d->sub = sub;
+    atomicOr(&d->flag, 1);
+}
+
+__device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
+
+// Accessor over the staged HBM arrays at one point.
+template <class T, class QS, class PT>
+struct GlobalAcc {
+    const QS* q;
+    const PT* prim;
+    const T* lev2;
+    long long plane;
+    long long fstride;  // prim/lev2 field stride
+    int nx;
+    int x, y, p;
+    int wx[5], wy[5];
+
+    __device__ __forceinline__ long long cell(int d, int s, int& pp) const {
+        const int xx = d == 0 ? wx[s + 2] : x;
+        const int yy = d == 1 ? wy[s + 2] : y;
+        pp = d == 2 ? p + s : p;
+        return (long long)yy * nx + xx;
+    }
+    __device__ __forceinline__ T Q(int c, int d, int s) const {
+        int pp;
+        const long long o = cell(d, s, pp);
+        return cvt<T>(q[(long long)(pp * 5 + c) * plane + o]);
+    }
+    __device__ __forceinline__ T F(int f, int d, int s) const {
+        int pp;
+        const long long o = cell(d, s, pp);
+        return cvt<T>(prim[f * fstride + pp * plane + o]);
+    }
+    __device__ __forceinline__ T U(int m, int d, int s) const { return F(m, d, s); }
+    __device__ __forceinline__ T P(int d, int s) const { return F(3, d, s); }
+    __device__ __forceinline__ T L(int f, int d, int s) const {
+        int pp;
+        const long long o = cell(d, s, pp);
+        return lev2[f * fstride + pp * plane + o];
+    }
+    __device__ __forceinline__ T DIVU(int d, int s) const { return L(0, d, s); }
+    __device__ __forceinline__ T G(int j, int d, int s) const { return L(1 + j, d, s); }
+    __device__ __forceinline__ T DT(int j, int d, int s) const { return L(4 + j, d, s); }
+};
+
+template <class T, class QS, class PT>
+__device__ __forceinline__ GlobalAcc<T, QS, PT> make_acc(const Geo& g, const QS* q, const PT* prim,
+                                                         const T* lev2, int x, int y, int p) {
+    GlobalAcc<T, QS, PT> a;
+    a.q = q;
+    a.prim = prim;
+    a.lev2 = lev2;
+    a.plane = g.plane;
+    a.fstride = (long long)g.planes * g.plane;
+    a.nx = g.nx;
+    a.x = x;
+    a.y = y;
+    a.p = p;
+#pragma unroll
+    for (int s = -2; s <= 2; ++s) {
+        a.wx[s + 2] = wrapi(x + s, g.nx);
+        a.wy[s + 2] = wrapi(y + s, g.ny);
+    }
+    return a;
+}
+
+struct PrimConsts {
+    double half, gm1, gM2;
+    int kind[5];  // storage kinds of u v w p T
+};
+
+// primitives_impl (physics.cpp:281-331) at wk compute WC, over every Q plane
+// (ghosts included, so the residual's z-stencils find them); the density
+// signal is raised for interior points only, first in scan order.
+template <class QS, class WC, class PT>
+__global__ void __launch_bounds__(256) k_prim(Geo g, const QS* __restrict__ q, PT* __restrict__ prim,
+                                              PrimConsts pc, DevDiv* div, int iter, int sub) {
+    if (div->flag) return;
+    using O = Op<WC>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int p = blockIdx.z;
+    if (x >= g.nx || y >= g.ny) return;
+    const long long o = (long long)y * g.nx + x;
+    const QS* qp = q + (long long)p * 5 * g.plane + o;
+    const WC rho = cvt<WC>(qp[0]);
+    if (p >= kHalo && p < g.nzl + kHalo) {
+        const float rf = (float)cvt<double>(rho);
+        if (!(rf > 0.0f) || !isfinite(rf)) {
+            const unsigned long long gi =
+                ((unsigned long long)(g.z0 + p - kHalo) * g.ny + y) * g.nx + x;
+            record_div(div, 0, 0, gi, iter, sub);
+        }
+    }
+    const WC half = cvt<WC>(pc.half), gm1 = cvt<WC>(pc.gm1), gM2 = cvt<WC>(pc.gM2);
+    const WC ux = O::div(cvt<WC>(qp[g.plane]), rho);
+    const WC uy = O::div(cvt<WC>(qp[2 * g.plane]), rho);
+    const WC uz = O::div(cvt<WC>(qp[3 * g.plane]), rho);
+    const WC Et = O::div(cvt<WC>(qp[4 * g.plane]), rho);
+    const WC kin = O::mul(half, O::add(O::add(O::mul(ux, ux), O::mul(uy, uy)), O::mul(uz, uz)));
+    const WC e = O::sub(Et, kin);
+    const WC pr = O::mul(gm1, O::mul(rho, e));
+    const WC Tv = O::div(O::mul(gM2, pr), rho);
+    const long long fs = (long long)g.planes * g.plane;
+    PT* out = prim + (long long)p * g.plane + o;
+    out[0] = cvt<PT>(round_kind<WC>(pc.kind[0], ux));
+    out[fs] = cvt<PT>(round_kind<WC>(pc.kind[1], uy));
+    out[2 * fs] = cvt<PT>(round_kind<WC>(pc.kind[2], uz));
+    out[3 * fs] = cvt<PT>(round_kind<WC>(pc.kind[3], pr));
+    out[4 * fs] = cvt<PT>(round_kind<WC>(pc.kind[4], Tv));
+}
+
+struct StageConsts {
+    double r_stage;  // cvt_wk(1/(12h)) for ddx1 staging (stencil.cpp:16)
+    int kind[12];    // storage kinds of dudx..dwdz, dTdx..dTdz
+};
+
+// level-2 viscous fields on planes [H-2, nzl+H+2): gradients (inline d1 in
+// residual precision for Storesome; wk-precision ddx1 rounded to the staged
+// arrays' storage for Default), then divu, sum_i u_i tau_ij, dT_j.
+template <class T, class WC, class PT, bool STAGED>
+__global__ void __launch_bounds__(256) k_level2(Geo g, const PT* __restrict__ prim, T* __restrict__ lev2,
+                                                ResConsts rc_, StageConsts sc, DevDiv* div) {
+    if (div->flag) return;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int p = blockIdx.z + kHalo - 2;
+    if (x >= g.nx || y >= g.ny) return;
+    const RC<T> c(rc_);
+    const auto a = make_acc<T, double, PT>(g, nullptr, prim, nullptr, x, y, p);
+    T G[9], dT[3], u[3];
+    if (!STAGED) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) G[i * 3 + j] = d1<T>([&](int s) { return a.U(i, j, s); }, c.r);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) dT[j] = d1<T>([&](int s) { return a.F(4, j, s); }, c.r);
+    } else {
+        const auto aw = make_acc<WC, double, PT>(g, nullptr, prim, nullptr, x, y, p);
+        const WC rw = cvt<WC>(sc.r_stage);
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const WC v = d1<WC>([&](int s) { return aw.U(i, j, s); }, rw);
+                G[i * 3 + j] = cvt<T>(round_kind<WC>(sc.kind[i * 3 + j], v));
+            }
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const WC v = d1<WC>([&](int s) { return aw.F(4, j, s); }, rw);
+            dT[j] = cvt<T>(round_kind<WC>(sc.kind[9 + j], v));
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) u[i] = a.U(i, 0, 0);
+    T divu, gg[3];
+    level2_point<T>(c, G, u, divu, gg);
+    const long long fs = (long long)g.planes * g.plane;
+    T* out = lev2 + (long long)p * g.plane + (long long)y * g.nx + x;
+    out[0] = divu;
+    out[fs] = gg[0];
+    out[2 * fs] = gg[1];
+    out[3 * fs] = gg[2];
+    out[4 * fs] = dT[0];
+    out[5 * fs] = dT[1];
+    out[6 * fs] = dT[2];
+}
+
+// the fused residual on interior planes; stores round to R storage and the
+// nonfinite-residual signal is raised per component, first in scan order
+template <class T, class QS, class PT, class RS>
+__global__ void __launch_bounds__(256) k_resid(Geo g, const QS* __restrict__ q, const PT* __restrict__ prim,
+                                               const T* __restrict__ lev2, RS* __restrict__ r,
+                                               ResConsts rc_, DevDiv* div, int iter, int sub) {
+    if (div->flag) return;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int z = blockIdx.z;
+    if (x >= g.nx || y >= g.ny) return;
+    const RC<T> c(rc_);
+    const auto a = make_acc<T, QS, PT>(g, q, prim, lev2, x, y, z + kHalo);
+    T out[5];
+    residual_point<T>(c, a, out);
+    const long long o = (long long)y * g.nx + x;
+    RS* rp = r + (long long)z * 5 * g.plane + o;
+#pragma unroll
+    for (int comp = 0; comp < 5; ++comp) {
+        const RS v = cvt<RS>(out[comp]);
+        rp[comp * g.plane] = v;
+        if (!isfinite(cvt<double>(v))) {
+            const unsigned long long gi = ((unsigned long long)(g.z0 + z) * g.ny + y) * g.nx + x;
+            record_div(div, 1, comp, gi, iter, sub);
+        }
+    }
+}
+
+struct RkConsts {
+    double a_c, dt_c, b_c;  // cvt'd at rk / q compute (integrate.cpp:59-60, 78)
+    int skip_a;             // a_i == 0.0 in binary64 (integrate.cpp:61)
+};
+
+// rk_substep (integrate.cpp:47-91): Qt at rk compute TC, Q at q compute QC.
+// The two reference passes are pointwise, so fusing them per point is
+// bitwise neutral.  Q is updated in place (interior planes only).
+template <class QS, class TS, class RS, class TC, class QC>
+__global__ void __launch_bounds__(256) k_rk(Geo g, QS* __restrict__ q, TS* __restrict__ qt,
+                                            const RS* __restrict__ r, RkConsts kc, DevDiv* div, int iter,
+                                            int sub) {
+    if (div->flag) return;
+    const long long n = (long long)g.nzl * g.plane;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int z = (int)(i / g.plane);
+    const long long o = i - (long long)z * g.plane;
+    const TC a_c = cvt<TC>(kc.a_c), dt_c = cvt<TC>(kc.dt_c);
+    const QC b_c = cvt<QC>(kc.b_c);
+#pragma unroll
+    for (int comp = 0; comp < 5; ++comp) {
+        const long long ir = ((long long)z * 5 + comp) * g.plane + o;
+        const long long iq = ((long long)(z + kHalo) * 5 + comp) * g.plane + o;
+        const TC t = Op<TC>::mul(dt_c, cvt<TC>(r[ir]));
+        const TC v = kc.skip_a ? t : Op<TC>::add(Op<TC>::mul(a_c, cvt<TC>(qt[ir])), t);
+        const TS vs = cvt<TS>(v);
+        qt[ir] = vs;
+        const QC nq = Op<QC>::add(cvt<QC>(q[iq]), Op<QC>::mul(b_c, cvt<QC>(vs)));
+        const QS ns = cvt<QS>(nq);
+        q[iq] = ns;
+        if (!isfinite(cvt<double>(ns))) {
+            const unsigned long long gi =
+                ((unsigned long long)(g.z0 + z) * g.ny + (o / g.nx)) * g.nx + (o % g.nx);
+            record_div(div, 2, comp, gi, iter, sub);
+        }
+    }
+}
+
+// --- diagnostics (tgv.cpp:83-175), binary64 on the widened carriers -----
+
+// integrand: which = 0 kinetic energy (plain / density weighted),
+// which = 1 |curl u|^2 with the binary64 d1 stencil (r = 1/(12h) uncvt'd)
+template <class QS>
+__global__ void __launch_bounds__(256) k_diag_integrand(Geo g, const QS* __restrict__ q, double* __restrict__ out,
+                                                        int which, int density, double r) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int z = blockIdx.z;
+    if (x >= g.nx || y >= g.ny) return;
+    const long long o = (long long)y * g.nx + x;
+    double val;
+    if (which == 0) {
+        const QS* qp = q + (long long)(z + kHalo) * 5 * g.plane + o;
+        const double rho = cvt<double>(qp[0]);
+        const double u = __ddiv_rn(cvt<double>(qp[g.plane]), rho);
+        const double v = __ddiv_rn(cvt<double>(qp[2 * g.plane]), rho);
+        const double w = __ddiv_rn(cvt<double>(qp[3 * g.plane]), rho);
+        const double k2 =
+            __dmul_rn(0.5, __dadd_rn(__dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v)), __dmul_rn(w, w)));
+        val = density ? __dmul_rn(rho, k2) : k2;
+    } else {
+        // velocity component m at offset s along axis d
+        auto vel = [&](int m, int d, int s) {
+            int xx = x, yy = y, pp = z + kHalo;
+            if (d == 0) xx = wrapi(x + s, g.nx);
+            else if (d == 1) yy = wrapi(y + s, g.ny);
+            else pp += s;
+            const QS* qp = q + (long long)pp * 5 * g.plane + (long long)yy * g.nx + xx;
+            return __ddiv_rn(cvt<double>(qp[(1 + m) * g.plane]), cvt<double>(qp[0]));
+        };
+        auto D1 = [&](int m, int d) {
+            return d1v<double>(vel(m, d, -2), vel(m, d, -1), vel(m, d, 1), vel(m, d, 2), r);
+        };
+        const double wx = __dsub_rn(D1(2, 1), D1(1, 2));
+        const double wy = __dsub_rn(D1(0, 2), D1(2, 0));
+        const double wz = __dsub_rn(D1(1, 0), D1(0, 1));
+        val = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz));
+    }
+    out[(long long)z * g.plane + o] = val;
+}
+
+// pairwise_sum of 4096-element chunks (reduce.cpp:14-22): 128 sequential
+// leaves of 32, then a perfect binary tree.  One warp per chunk: each lane
+// owns 4 consecutive leaves, the lane tree is a xor butterfly (IEEE addition
+// is commutative, so both partners hold the same bits).
+__global__ void k_chunk_sums(const double* __restrict__ v, long long nchunks, double* __restrict__ out) {
+    const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nchunks) return;
+    const double* base = v + w * 4096 + lane * 128;
+    double leaf[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+        double s = 0.0;
+        for (int i = 0; i < 32; ++i) s = __dadd_rn(s, base[l * 32 + i]);
+        leaf[l] = s;
+    }
+    double acc = __dadd_rn(__dadd_rn(leaf[0], leaf[1]), __dadd_rn(leaf[2], leaf[3]));
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+    if (lane == 0) out[w] = acc;
+}
+
+}  // namespace mpfd_b200

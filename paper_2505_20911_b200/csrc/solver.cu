@@ -1,0 +1,1424 @@
+// solver.cu -- host runtime of the B200 TGV time step and its C-ABI
+// (include/mpfd_b200.h).
+//
+// One solver owns one or more z-slabs.  Each slab lives on one device with its
+// own stream and HBM arrays (kernels_staged.cuh has the layout).  Halos move
+// by device copies between slabs of this process (MPFD_DECOMP_LOCAL) or by
+// NCCL send/recv between processes (MPFD_DECOMP_NCCL, one slab per rank), in
+// the q_vector storage precision.
+//
+// Reference interfaces replaced:
+//   make_solver_fields physics.cpp:441-475   -> Solver::Solver
+//   init_tgv/init_uniform tgv.cpp:29-74       -> Solver::init
+//   ResidualEvaluator::evaluate :485-587      -> Solver::residual
+//   rk_substep integrate.cpp:47-91            -> Solver::rk_substep
+//   fill_state_halos integrate.cpp:93-95      -> Solver::halo_refresh
+//   advance integrate.cpp:97-167              -> Solver::advance
+//   DiagnosticsComputer tgv.cpp:76-175        -> Solver::diagnostics
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstdio>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/mpfd_b200.h"
+#include "host_common.hpp"
+#include "kernels_fused.cuh"
+#include "kernels_staged.cuh"
+
+namespace mpfd_b200 {
+
+static thread_local std::string g_err;
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            throw DeviceError(std::string(#call) + ": " + cudaGetErrorString(e_) + " at " + \
+                              __FILE__ + ":" + std::to_string(__LINE__));                     \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded on demand (only MPFD_DECOMP_NCCL needs it)
+struct Nccl {
+    typedef int (*GetUniqueId)(void*);
+    typedef int (*CommInitRank)(void**, int, const void* /*by value struct*/, int);
+    void* lib = nullptr;
+    int (*getUniqueId)(void*) = nullptr;
+    int (*commInitRank)(void**, int, char[128], int) = nullptr;
+    int (*commDestroy)(void*) = nullptr;
+    int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*groupStart)() = nullptr;
+    int (*groupEnd)() = nullptr;
+    int (*allGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+    int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    const char* (*errStr)(int) = nullptr;
+
+    static Nccl& get() {
+        static Nccl n;
+        if (!n.lib) {
+            n.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+            if (!n.lib) throw DeviceError(std::string("cannot load libnccl.so.2: ") + dlerror());
+            auto sym = [&](const char* s) {
+                void* p = dlsym(n.lib, s);
+                if (!p) throw DeviceError(std::string("NCCL symbol missing: ") + s);
+                return p;
+            };
+            n.getUniqueId = (int (*)(void*))sym("ncclGetUniqueId");
+            n.commInitRank = (int (*)(void**, int, char[128], int))sym("ncclCommInitRank");
+            n.commDestroy = (int (*)(void*))sym("ncclCommDestroy");
+            n.send = (int (*)(const void*, size_t, int, int, void*, cudaStream_t))sym("ncclSend");
+            n.recv = (int (*)(void*, size_t, int, int, void*, cudaStream_t))sym("ncclRecv");
+            n.groupStart = (int (*)())sym("ncclGroupStart");
+            n.groupEnd = (int (*)())sym("ncclGroupEnd");
+            n.allGather = (int (*)(const void*, void*, size_t, int, void*, cudaStream_t))sym("ncclAllGather");
+            n.allReduce =
+                (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))sym("ncclAllReduce");
+            n.errStr = (const char* (*)(int))sym("ncclGetErrorString");
+        }
+        return n;
+    }
+    void check(int r, const char* what) const {
+        if (r != 0) throw DeviceError(std::string(what) + ": " + errStr(r));
+    }
+};
+// ncclDataType_t values (nccl.h): ncclUint8 1, ncclInt32 2, ncclUint64 5, ncclFloat64 8
+// ncclRedOp_t: ncclSum 0, ncclMin 3
+
+template <int K>
+struct TypeOfK;
+template <>
+struct TypeOfK<0> {
+    using type = __half;
+};
+template <>
+struct TypeOfK<1> {
+    using type = float;
+};
+template <>
+struct TypeOfK<2> {
+    using type = double;
+};
+template <int K>
+using TypeOf = typename TypeOfK<K>::type;
+
+// ---------------------------------------------------------------------------
+// per-slab device state
+struct Slab {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    Geo geo{};
+    void* q = nullptr;     // [planes][5][ny][nx] QS
+    void* qt = nullptr;    // [nzl][5][ny][nx]   TS
+    void* r = nullptr;     // [nzl][5][ny][nx]   RS
+    void* q2 = nullptr;    // fused path: Q output buffer (double-buffered)
+    void* qt2 = nullptr;   // fused path: Qt output buffer
+    void* prim = nullptr;  // staged path
+    void* lev2 = nullptr;  // staged path
+    double* diag = nullptr;
+    double* partials = nullptr;
+    DevDiv* div = nullptr;
+    double* staging = nullptr;
+    size_t staging_elems = 0;
+    size_t bytes = 0;
+};
+
+struct KernelPlan {
+    int mode;
+    int qk, tk, rk, wk;  // storage kinds of Q, Qt, R and the wk class
+    int pk;              // staged primitives buffer kind
+};
+
+// launch tables, one instantiation per supported precision plan
+struct Launcher {
+    virtual ~Launcher() = default;
+    virtual void prim(const Slab& s, const PrimConsts& pc, int iter, int sub) = 0;
+    virtual void level2(const Slab& s, const ResConsts& rc, const StageConsts& sc, bool staged) = 0;
+    virtual void resid(const Slab& s, const ResConsts& rc, int iter, int sub) = 0;
+    virtual void rk(const Slab& s, const RkConsts& kc, int iter, int sub) = 0;
+    virtual void diag_integrand(const Slab& s, int which, int density, double r) = 0;
+    virtual bool fused_available() const = 0;
+    virtual void fused(const Slab& s, const void* qin, void* qout, const void* qtin, void* qtout,
+                       const PrimConsts& pc, const ResConsts& rc, const StageConsts& sc, bool staged,
+                       const RkConsts& kc, bool write_r, int iter, int sub) = 0;
+};
+
+static dim3 block2d() { return dim3(32, 8, 1); }
+static dim3 grid2d(const Geo& g, int planes) {
+    return dim3((unsigned)((g.nx + 31) / 32), (unsigned)((g.ny + 7) / 8), (unsigned)planes);
+}
+
+template <int MODE, int QK, int TK, int RK, int WK, int PK>
+struct LauncherT final : Launcher {
+    using QS = TypeOf<QK>;
+    using TS = TypeOf<TK>;
+    using RS = TypeOf<RK>;
+    using PT = TypeOf<PK>;
+    using WC = TypeOf<MODE == 0 ? WK : 2>;
+    using RCt = TypeOf<MODE == 0 ? RK : 2>;
+    using TC = TypeOf<MODE == 0 ? TK : 2>;
+    using QC = TypeOf<MODE == 0 ? QK : 2>;
+
+    void prim(const Slab& s, const PrimConsts& pc, int iter, int sub) override {
+        k_prim<QS, WC, PT><<<grid2d(s.geo, s.geo.planes), block2d(), 0, s.stream>>>(
+            s.geo, (const QS*)s.q, (PT*)s.prim, pc, s.div, iter, sub);
+    }
+    void level2(const Slab& s, const ResConsts& rc, const StageConsts& sc, bool staged) override {
+        if (staged)
+            k_level2<RCt, WC, PT, true><<<grid2d(s.geo, s.geo.nzl + 4), block2d(), 0, s.stream>>>(
+                s.geo, (const PT*)s.prim, (RCt*)s.lev2, rc, sc, s.div);
+        else
+            k_level2<RCt, WC, PT, false><<<grid2d(s.geo, s.geo.nzl + 4), block2d(), 0, s.stream>>>(
+                s.geo, (const PT*)s.prim, (RCt*)s.lev2, rc, sc, s.div);
+    }
+    void resid(const Slab& s, const ResConsts& rc, int iter, int sub) override {
+        k_resid<RCt, QS, PT, RS><<<grid2d(s.geo, s.geo.nzl), block2d(), 0, s.stream>>>(
+            s.geo, (const QS*)s.q, (const PT*)s.prim, (const RCt*)s.lev2, (RS*)s.r, rc, s.div, iter, sub);
+    }
+    void rk(const Slab& s, const RkConsts& kc, int iter, int sub) override {
+        const long long n = (long long)s.geo.nzl * s.geo.plane;
+        k_rk<QS, TS, RS, TC, QC><<<(unsigned)((n + 255) / 256), 256, 0, s.stream>>>(
+            s.geo, (QS*)s.q, (TS*)s.qt, (const RS*)s.r, kc, s.div, iter, sub);
+    }
+    void diag_integrand(const Slab& s, int which, int density, double r) override {
+        k_diag_integrand<QS><<<grid2d(s.geo, s.geo.nzl), block2d(), 0, s.stream>>>(
+            s.geo, (const QS*)s.q, s.diag, which, density, r);
+    }
+    bool fused_available() const override { return FusedPlan<MODE, QK, TK, RK, WK>::available; }
+    void fused(const Slab& s, const void* qin, void* qout, const void* qtin, void* qtout,
+               const PrimConsts& pc, const ResConsts& rc, const StageConsts& sc, bool staged,
+               const RkConsts& kc, bool write_r, int iter, int sub) override {
+        FusedPlan<MODE, QK, TK, RK, WK>::launch(s.geo, s.stream, qin, qout, qtin, qtout, s.r, pc, rc, sc,
+                                                staged, kc, write_r, s.div, iter, sub);
+    }
+};
+
+// supported precision plans: the reference's nine presets under both
+// emulation modes (precision.cpp:58-88).  mode, q, rk, res, wk, prim buffer.
+#define MPFD_PLANS(X)        \
+    X(0, 2, 2, 2, 2, 2)      \
+    X(0, 1, 1, 1, 1, 1)      \
+    X(0, 0, 0, 0, 0, 0)      \
+    X(0, 2, 2, 1, 1, 1)      \
+    X(0, 2, 2, 2, 1, 1)      \
+    X(0, 2, 2, 1, 2, 2)      \
+    X(0, 1, 1, 0, 0, 0)      \
+    X(0, 1, 1, 1, 0, 0)      \
+    X(0, 1, 1, 0, 1, 1)      \
+    X(1, 2, 2, 2, 2, 2)      \
+    X(1, 1, 1, 1, 1, 1)      \
+    X(1, 0, 0, 0, 0, 0)      \
+    X(1, 2, 2, 1, 1, 1)      \
+    X(1, 2, 2, 2, 1, 1)      \
+    X(1, 2, 2, 1, 2, 2)      \
+    X(1, 1, 1, 0, 0, 0)      \
+    X(1, 1, 1, 1, 0, 0)      \
+    X(1, 1, 1, 0, 1, 1)
+
+static std::unique_ptr<Launcher> make_launcher(const KernelPlan& p) {
+#define MPFD_TRY(m, q, t, r, w, pbuf)                                                         \
+    if (p.mode == m && p.qk == q && p.tk == t && p.rk == r && p.wk == w && p.pk == pbuf)      \
+        return std::unique_ptr<Launcher>(new LauncherT<m, q, t, r, w, pbuf>());
+    MPFD_PLANS(MPFD_TRY)
+#undef MPFD_TRY
+    return nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// host reductions (reduce.cpp:14-36)
+static double pairwise_sum(const double* v, size_t n) {
+    if (n <= 32) {
+        double s = 0.0;
+        for (size_t i = 0; i < n; ++i) s += v[i];
+        return s;
+    }
+    const size_t h = n / 2;
+    return pairwise_sum(v, h) + pairwise_sum(v + h, n - h);
+}
+// pure pairwise over N = nchunks*4096 elements given the chunk sums: valid
+// when nchunks is a power of two (the halving tree meets chunk boundaries)
+static double tree_of_chunks(const double* c, size_t n) {
+    if (n == 1) return c[0];
+    const size_t h = n / 2;
+    return tree_of_chunks(c, h) + tree_of_chunks(c + h, n - h);
+}
+
+// ---------------------------------------------------------------------------
+struct Solver {
+    // configuration
+    int n = 0;
+    double L = 0.0, h = 0.0;
+    Precision prec;
+    int strategy = 0;
+    double mach = 0.1, re = 1600.0, pr = 0.72, gamma = 1.4;
+    int viscous = 1;
+    double w[7] = {0};
+    int pz = 1, mode = MPFD_DECOMP_LOCAL, rank = 0;
+    int kinds_prim[5]{}, kinds_grad[12]{};
+    KernelPlan plan{};
+    std::unique_ptr<Launcher> launch;
+    std::vector<Slab> slabs;
+    void* comm = nullptr;
+    int path = 1;  // 1 fused when available, 0 staged
+    bool halo_fresh = false;
+    int qbuf = 0;  // fused path: which Q/Qt buffer holds the state
+    // timing
+    bool profiling = false;
+    double prof_ms[4] = {0, 0, 0, 0};
+    long prof_launch[4] = {0, 0, 0, 0};
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[4];
+    std::vector<cudaEvent_t> event_pool;
+    int* pinned_flag = nullptr;
+
+    ~Solver();
+    void setup(const mpfd_grid* grid, const mpfd_precision* p, int strategy_, const mpfd_flow* flow,
+               const mpfd_split* sp, const mpfd_decomp* dc);
+    void alloc();
+    void reset_div();
+
+    int nzl() const { return slabs.empty() ? 0 : slabs[0].geo.nzl; }
+    bool use_fused() const { return path == 1 && launch->fused_available(); }
+    void* qcur(const Slab& s) const { return (use_fused() && qbuf) ? s.q2 : s.q; }
+    void* qtcur(const Slab& s) const { return (use_fused() && qbuf) ? s.qt2 : s.qt; }
+
+    // constants
+    PrimConsts prim_consts() const;
+    ResConsts res_consts() const;
+    StageConsts stage_consts() const;
+    RkConsts rk_consts(int sub, const double a[3], const double b[3], double dt) const;
+
+    // operations
+    void init(int case_kind);
+    void set_interior(int cls, int comp, const double* src, size_t ld_row, size_t ld_plane, int off);
+    void upload_slab(Slab& s, int cls, int comp, const double* src, size_t ld_row, size_t ld_plane);
+    void get_interior(int cls, int comp, double* dst, size_t ld_row, size_t ld_plane, int off);
+    void halo_refresh();
+    void residual_enqueue(int iter, int sub);
+    void rk_enqueue(int sub, const double a[3], const double b[3], double dt, int iter);
+    void substep_enqueue(int sub, const double a[3], const double b[3], double dt, int iter, bool write_r);
+    bool poll_div(bool block);
+    bool resolve_div(mpfd_divergence* ev, double dt);
+    void diagnostics(int weighting, double t, int threads, mpfd_diag* out);
+    void sync();
+    template <class F>
+    void timed(int cls, const Slab& s, F&& f);
+    void begin_profile_window();
+    void flush_profile();
+};
+
+Solver::~Solver() {
+    for (auto& s : slabs) {
+        cudaSetDevice(s.device);
+        for (void* p : {s.q, s.qt, s.r, s.q2, s.qt2, s.prim, s.lev2}) cudaFree(p);
+        cudaFree(s.diag);
+        cudaFree(s.partials);
+        cudaFree(s.div);
+        cudaFree(s.staging);
+        if (s.stream) cudaStreamDestroy(s.stream);
+    }
+    for (auto& v : prof_ev)
+        for (auto& e : v) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+    if (pinned_flag) cudaFreeHost(pinned_flag);
+    if (comm) Nccl::get().commDestroy(comm);
+}
+
+void Solver::setup(const mpfd_grid* grid, const mpfd_precision* p, int strategy_, const mpfd_flow* flow,
+                   const mpfd_split* sp, const mpfd_decomp* dc) {
+    if (!grid || !p || !flow || !sp) throw ConfigError("null configuration pointer");
+    n = grid->n;
+    if (n < 5) throw ConfigError("GridSpec: n must be >= 5");
+    L = grid->domain_length > 0 ? grid->domain_length : 2.0 * 3.14159265358979323846;
+    h = L / n;
+    prec.q = p->q_vector;
+    prec.rk = p->rk_arrays;
+    prec.res = p->residuals;
+    prec.wk = p->wk_arrays;
+    prec.emulation = p->emulation;
+    for (int k : {prec.q, prec.rk, prec.res, prec.wk})
+        if (k < 0 || k > 2) throw ConfigError("precision kind out of range");
+    for (int i = 0; i < p->n_overrides; ++i) {
+        const int k = p->override_kinds[i];
+        if (k < 0 || k > 2) throw ConfigError("override kind out of range");
+        prec.overrides[p->override_names[i]] = k;
+    }
+    strategy = strategy_;
+    mach = flow->mach;
+    re = flow->reynolds;
+    pr = flow->prandtl;
+    gamma = flow->gamma;
+    viscous = flow->viscous != 0;
+    // FlowParams::validate (physics.cpp:9-14)
+    if (!(mach > 0.0)) throw ConfigError("FlowParams: M must be positive");
+    if (viscous && !(re > 0.0)) throw ConfigError("FlowParams: Re must be positive");
+    if (!(pr > 0.0)) throw ConfigError("FlowParams: Pr must be positive");
+    if (!(gamma > 1.0)) throw ConfigError("FlowParams: gamma must exceed 1");
+    const double ww[7] = {sp->alpha, sp->beta_rho, sp->beta_u, sp->beta_phi,
+                          sp->gamma_rho, sp->gamma_u, sp->gamma_phi};
+    for (int i = 0; i < 7; ++i) w[i] = ww[i];
+    // SplitCoefficients::is_consistent (physics.hpp:49-58)
+    if (!(w[0] + w[2] + w[3] + w[4] == 1.0 && w[0] + w[1] + w[3] + w[5] == 1.0 &&
+          w[0] + w[1] + w[2] + w[6] == 1.0))
+        throw ConfigError("split coefficients violate the consistency constraints");
+
+    // per-class homogeneous storage for the HBM-resident Q, Qt, R
+    for (int c = 0; c < 5; ++c) {
+        if (prec.resolve(0, kQNames[c]) != prec.q || prec.resolve(1, kTNames[c]) != prec.rk ||
+            prec.resolve(2, kRNames[c]) != prec.res)
+            throw ConfigError(
+                "B200 backend: per-component overrides of q_vector/rk_arrays/residuals are not "
+                "supported (HBM layout is one precision per class)");
+    }
+    int pk = prec.wk;
+    for (int i = 0; i < 5; ++i) {
+        kinds_prim[i] = prec.resolve(3, kPNames[i]);
+        pk = std::max(pk, kinds_prim[i]);
+    }
+    for (int i = 0; i < 12; ++i) kinds_grad[i] = prec.resolve(3, kGNames[i]);
+    // staged primitive buffer: exact carrier of every stored primitive
+    plan = {prec.emulation, prec.q, prec.rk, prec.res, prec.wk,
+            prec.emulation == 0 ? prec.wk : pk};
+    launch = make_launcher(plan);
+    if (!launch)
+        throw ConfigError("B200 backend: precision combination not compiled (supported: the nine "
+                          "presets DP SP HP SPDP SPDP-wk SPDP-res HPSP HPSP-wk HPSP-res, strict or "
+                          "storeround)");
+
+    // decomposition
+    mpfd_decomp d{1, MPFD_DECOMP_LOCAL, 0, 0, nullptr, nullptr};
+    if (dc) d = *dc;
+    pz = d.pz < 1 ? 1 : d.pz;
+    mode = d.mode;
+    rank = d.rank;
+    if (n % pz != 0) throw ConfigError("grid n is not divisible by the z process count");
+    if (n / pz < kHalo) throw ConfigError("z slab thinner than the halo depth (4)");
+    const int nz_local = n / pz;
+    const int nslab = mode == MPFD_DECOMP_NCCL ? 1 : pz;
+    slabs.resize(nslab);
+    for (int i = 0; i < nslab; ++i) {
+        Slab& s = slabs[i];
+        s.device = (mode == MPFD_DECOMP_LOCAL && d.devices) ? d.devices[i] : d.device;
+        const int r = mode == MPFD_DECOMP_NCCL ? rank : i;
+        s.geo.nx = n;
+        s.geo.ny = n;
+        s.geo.nzl = nz_local;
+        s.geo.z0 = r * nz_local;
+        s.geo.plane = (long long)n * n;
+        s.geo.planes = nz_local + 2 * kHalo;
+    }
+    if (mode == MPFD_DECOMP_NCCL && pz > 1) {
+        if (!d.nccl_id) throw ConfigError("NCCL decomposition needs nccl_id");
+        CK(cudaSetDevice(slabs[0].device));
+        char id[128];
+        std::memcpy(id, d.nccl_id, 128);
+        Nccl& nc = Nccl::get();
+        nc.check(nc.commInitRank(&comm, pz, id, rank), "ncclCommInitRank");
+    }
+    alloc();
+}
+
+void Solver::alloc() {
+    const size_t bq = byte_width(plan.qk), bt = byte_width(plan.tk), br = byte_width(plan.rk);
+    const size_t bp = byte_width(plan.pk);
+    const size_t bl = byte_width(plan.mode == 0 ? plan.rk : 2);
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+        const size_t pl = (size_t)s.geo.plane;
+        const size_t qel = (size_t)s.geo.planes * 5 * pl;
+        const size_t iel = (size_t)s.geo.nzl * 5 * pl;
+        auto get = [&](void** p, size_t bytes) {
+            CK(cudaMalloc(p, bytes));
+            CK(cudaMemsetAsync(*p, 0, bytes, s.stream));
+            s.bytes += bytes;
+        };
+        get(&s.q, qel * bq);
+        get(&s.qt, iel * bt);
+        get(&s.r, iel * br);
+        if (launch->fused_available()) {
+            get(&s.q2, qel * bq);
+            get(&s.qt2, iel * bt);
+        }
+        CK(cudaMalloc(&s.div, sizeof(DevDiv)));
+        s.bytes += sizeof(DevDiv);
+        const size_t nint = (size_t)s.geo.nzl * pl;
+        CK(cudaMalloc(&s.diag, nint * sizeof(double)));
+        CK(cudaMalloc(&s.partials, ((nint + 4095) / 4096) * sizeof(double)));
+        s.bytes += nint * sizeof(double) + ((nint + 4095) / 4096) * sizeof(double);
+        s.staging_elems = std::min<size_t>(nint, (size_t)1 << 26);
+        CK(cudaMalloc(&s.staging, s.staging_elems * sizeof(double)));
+        s.bytes += s.staging_elems * sizeof(double);
+    }
+    if (!launch->fused_available()) path = 0;
+    CK(cudaHostAlloc(&pinned_flag, sizeof(int) * 64, cudaHostAllocDefault));
+    reset_div();
+    sync();
+}
+
+static void alloc_staged(Solver& S) {
+    const size_t bp = byte_width(S.plan.pk);
+    const size_t bl = byte_width(S.plan.mode == 0 ? S.plan.rk : 2);
+    for (auto& s : S.slabs) {
+        if (s.prim) continue;
+        CK(cudaSetDevice(s.device));
+        const size_t el = (size_t)s.geo.planes * s.geo.plane;
+        CK(cudaMalloc(&s.prim, 5 * el * bp));
+        CK(cudaMalloc(&s.lev2, 7 * el * bl));
+        CK(cudaMemsetAsync(s.prim, 0, 5 * el * bp, s.stream));
+        CK(cudaMemsetAsync(s.lev2, 0, 7 * el * bl, s.stream));
+        s.bytes += 5 * el * bp + 7 * el * bl;
+    }
+}
+
+void Solver::reset_div() {
+    DevDiv d;
+    std::memset(&d, 0, sizeof d);
+    for (auto& row : d.idx)
+        for (auto& v : row) v = ULLONG_MAX;
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        CK(cudaMemcpyAsync(s.div, &d, sizeof d, cudaMemcpyHostToDevice, s.stream));
+        CK(cudaStreamSynchronize(s.stream));
+    }
+}
+
+void Solver::sync() {
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        CK(cudaStreamSynchronize(s.stream));
+    }
+}
+
+// A::cvt of the constants (physics.cpp:167-173, 288-290, 537-544;
+// stencil.cpp:16; integrate.cpp:59-61, 78)
+PrimConsts Solver::prim_consts() const {
+    const int c = prec.emulation == 0 ? prec.wk : B64;
+    PrimConsts pc;
+    pc.half = round_to(c, 0.5);
+    pc.gm1 = round_to(c, gamma - 1.0);
+    pc.gM2 = round_to(c, gamma * mach * mach);
+    for (int i = 0; i < 5; ++i) pc.kind[i] = kinds_prim[i];
+    return pc;
+}
+ResConsts Solver::res_consts() const {
+    const int c = prec.emulation == 0 ? prec.res : B64;
+    ResConsts rc;
+    rc.r = round_to(c, 1.0 / (12.0 * h));
+    rc.r2 = round_to(c, 1.0 / (12.0 * h * h));
+    rc.inv_re = round_to(c, 1.0 / re);
+    rc.third = round_to(c, 1.0 / 3.0);
+    rc.two_thirds = round_to(c, 2.0 / 3.0);
+    rc.kappa = round_to(c, 1.0 / ((gamma - 1.0) * mach * mach * re * pr));
+    rc.nz = 0;
+    for (int i = 0; i < 7; ++i) {
+        rc.coef[i] = round_to(c, w[i]);
+        if (w[i] != 0.0) rc.nz |= 1u << i;
+    }
+    rc.viscous = viscous;
+    return rc;
+}
+StageConsts Solver::stage_consts() const {
+    const int c = prec.emulation == 0 ? prec.wk : B64;
+    StageConsts sc;
+    sc.r_stage = round_to(c, 1.0 / (12.0 * h));
+    for (int i = 0; i < 12; ++i) sc.kind[i] = kinds_grad[i];
+    return sc;
+}
+RkConsts Solver::rk_consts(int sub, const double a[3], const double b[3], double dt) const {
+    const int tc = prec.emulation == 0 ? prec.rk : B64;
+    const int qc = prec.emulation == 0 ? prec.q : B64;
+    RkConsts kc;
+    kc.a_c = round_to(tc, a[sub]);
+    kc.dt_c = round_to(tc, dt);
+    kc.b_c = round_to(qc, b[sub]);
+    kc.skip_a = a[sub] == 0.0;
+    return kc;
+}
+
+// ---------------------------------------------------------------------------
+// host <-> device carriers: values are converted on the device from binary64
+// staging (one RNE rounding, Field::set field.hpp:77-80)
+
+template <class S>
+__global__ void k_from_double(const double* __restrict__ src, S* __restrict__ dst, long long count,
+                              long long dst_pitch_plane, long long plane_count_per) {
+    // src packed [plane][y][x]; dst plane stride dst_pitch_plane
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const long long pl = i / plane_count_per;
+    const long long o = i - pl * plane_count_per;
+    dst[pl * dst_pitch_plane + o] = cvt<S>(src[i]);
+}
+template <class S>
+__global__ void k_to_double(const S* __restrict__ src, double* __restrict__ dst, long long count,
+                            long long src_pitch_plane, long long plane_count_per) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const long long pl = i / plane_count_per;
+    const long long o = i - pl * plane_count_per;
+    dst[i] = cvt<double>(src[pl * src_pitch_plane + o]);
+}
+
+template <class F>
+static void with_kind(int k, F&& f) {
+    if (k == 0) f(__half{});
+    else if (k == 1) f(float{});
+    else f(double{});
+}
+
+// cls 0 Q, 1 Qt, 2 R.  src indexes this slab's local point (i,j,k) at
+// k*ld_plane + j*ld_row + i (binary64 carriers); rounded on the device
+void Solver::upload_slab(Slab& s, int cls, int comp, const double* src, size_t ld_row, size_t ld_plane) {
+    if (cls < 0 || cls > 2 || comp < 0 || comp > 4) throw ConfigError("bad class/component");
+    const int kind = cls == 0 ? plan.qk : (cls == 1 ? plan.tk : plan.rk);
+    CK(cudaSetDevice(s.device));
+    const long long pl = s.geo.plane;
+    const int planes_per = (int)std::max<size_t>(1, s.staging_elems / pl);
+    for (int z = 0; z < s.geo.nzl; z += planes_per) {
+        const int nzc = std::min(planes_per, s.geo.nzl - z);
+        for (int zz = 0; zz < nzc; ++zz)
+            CK(cudaMemcpy2DAsync(s.staging + (size_t)zz * pl, (size_t)n * sizeof(double),
+                                 src + (size_t)(z + zz) * ld_plane, ld_row * sizeof(double),
+                                 (size_t)n * sizeof(double), n, cudaMemcpyHostToDevice, s.stream));
+        void* base = cls == 0 ? qcur(s) : (cls == 1 ? qtcur(s) : s.r);
+        const long long count = (long long)nzc * pl;
+        const long long zoff = cls == 0 ? z + kHalo : z;
+        with_kind(kind, [&](auto tag) {
+            using S = decltype(tag);
+            S* dst = (S*)base + (zoff * 5 + comp) * pl;
+            k_from_double<S><<<(unsigned)((count + 255) / 256), 256, 0, s.stream>>>(s.staging, dst, count,
+                                                                                     5 * pl, pl);
+        });
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s.stream));
+    }
+    if (cls == 0) halo_fresh = false;
+}
+
+void Solver::set_interior(int cls, int comp, const double* src, size_t ld_row, size_t ld_plane, int off) {
+    for (auto& s : slabs) upload_slab(s, cls, comp, src + off + (size_t)s.geo.z0 * ld_plane, ld_row, ld_plane);
+}
+
+void Solver::get_interior(int cls, int comp, double* dst, size_t ld_row, size_t ld_plane, int off) {
+    if (cls < 0 || cls > 2 || comp < 0 || comp > 4) throw ConfigError("bad class/component");
+    const int kind = cls == 0 ? plan.qk : (cls == 1 ? plan.tk : plan.rk);
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        const long long pl = s.geo.plane;
+        const int planes_per = (int)std::max<size_t>(1, s.staging_elems / pl);
+        for (int z = 0; z < s.geo.nzl; z += planes_per) {
+            const int nzc = std::min(planes_per, s.geo.nzl - z);
+            const void* base = cls == 0 ? qcur(s) : (cls == 1 ? qtcur(s) : s.r);
+            const long long count = (long long)nzc * pl;
+            with_kind(kind, [&](auto tag) {
+                using S = decltype(tag);
+                const S* srcp = cls == 0 ? (const S*)base + ((long long)(z + kHalo) * 5 + comp) * pl
+                                         : (const S*)base + ((long long)z * 5 + comp) * pl;
+                k_to_double<S><<<(unsigned)((count + 255) / 256), 256, 0, s.stream>>>(srcp, s.staging,
+                                                                                       count, 5 * pl, pl);
+            });
+            CK(cudaGetLastError());
+            for (int zz = 0; zz < nzc; ++zz) {
+                const size_t kg = (size_t)(s.geo.z0 + z + zz);
+                CK(cudaMemcpy2DAsync(dst + off + kg * ld_plane, ld_row * sizeof(double),
+                                     s.staging + (size_t)zz * pl, (size_t)n * sizeof(double),
+                                     (size_t)n * sizeof(double), n, cudaMemcpyDeviceToHost, s.stream));
+            }
+        }
+        CK(cudaStreamSynchronize(s.stream));
+    }
+}
+
+// init_tgv (tgv.cpp:29-60) / init_uniform (tgv.cpp:62-74): binary64 on the
+// host with glibc sin/cos, exactly the reference's expressions
+void Solver::init(int case_kind) {
+    const double g = gamma, m = mach;
+    const double gm2 = g * m * m;
+    if (case_kind == 0 && std::abs(L - 2.0 * 3.14159265358979323846) > 1e-12)
+        throw ConfigError("init_tgv requires a (2 pi)^3 domain");
+    const size_t pl = (size_t)n * n;
+    const double h_ = h;
+    const double p_ref = 1.0 / gm2;
+    qbuf = 0;
+    for (auto& s : slabs) {
+        // this slab's planes only, [nzl][n][n]
+        const size_t z0 = (size_t)s.geo.z0, nzl_ = (size_t)s.geo.nzl;
+        std::vector<double> f[5];
+        for (auto& v : f) v.assign(nzl_ * pl, 0.0);
+        auto fill_planes = [&](size_t k0, size_t k1) {
+            for (size_t k = k0; k < k1; ++k) {
+                const double z = (double)(z0 + k) * h_;
+                for (int j = 0; j < n; ++j) {
+                    const double y = j * h_;
+                    for (int i = 0; i < n; ++i) {
+                        const size_t o = (k * n + j) * n + i;
+                        if (case_kind == 1) {
+                            const double p0 = 1.0 / gm2;
+                            f[0][o] = gm2 * p0;
+                            f[1][o] = f[2][o] = f[3][o] = 0.0;
+                            f[4][o] = p0 / (g - 1.0);
+                            continue;
+                        }
+                        const double x = i * h_;
+                        const double u = std::sin(x) * std::cos(y) * std::cos(z);
+                        const double v = -std::cos(x) * std::sin(y) * std::cos(z);
+                        const double p = p_ref + (1.0 / 16.0) * (std::cos(2 * x) + std::cos(2 * y)) *
+                                                     (2.0 + std::cos(2 * z));
+                        const double rho = gm2 * p;
+                        const double rhoE = p / (g - 1.0) + 0.5 * rho * (u * u + v * v);
+                        f[0][o] = rho;
+                        f[1][o] = rho * u;
+                        f[2][o] = rho * v;
+                        f[3][o] = 0.0;
+                        f[4][o] = rhoE;
+                    }
+                }
+            }
+        };
+        const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nt; ++t)
+            th.emplace_back(fill_planes, nzl_ * t / nt, nzl_ * (t + 1) / nt);
+        for (auto& t : th) t.join();
+        for (int comp = 0; comp < 5; ++comp) upload_slab(s, 0, comp, f[comp].data(), n, pl);
+    }
+    halo_fresh = false;
+    // Qt and R zeroed (zero_temporaries, tgv.cpp:22-25)
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        const size_t iel = (size_t)s.geo.nzl * 5 * s.geo.plane;
+        CK(cudaMemsetAsync(s.qt, 0, iel * byte_width(plan.tk), s.stream));
+        CK(cudaMemsetAsync(s.r, 0, iel * byte_width(plan.rk), s.stream));
+        if (s.qt2) CK(cudaMemsetAsync(s.qt2, 0, iel * byte_width(plan.tk), s.stream));
+    }
+    reset_div();
+    halo_refresh();
+    sync();
+}
+
+// fill_state_halos (integrate.cpp:93-95): ghost planes [0,H) <- the
+// z-previous slab's top H interior planes, [nzl+H, nzl+2H) <- the z-next
+// slab's bottom H interior planes (periodic ring).  One contiguous block of
+// H*5*ny*nx storage-precision values per direction.
+void Solver::halo_refresh() {
+    const size_t bq = byte_width(plan.qk);
+    if (mode == MPFD_DECOMP_NCCL && pz > 1) {
+        Slab& s = slabs[0];
+        CK(cudaSetDevice(s.device));
+        const size_t blk = (size_t)kHalo * 5 * s.geo.plane * bq;
+        char* q = (char*)qcur(s);
+        const int up = (rank + 1) % pz, dn = (rank + pz - 1) % pz;
+        char* top_int = q + (size_t)s.geo.nzl * 5 * s.geo.plane * bq;  // planes [nzl, nzl+H)
+        char* bot_int = q + blk;                                      // planes [H, 2H)
+        char* lo_ghost = q;                                           // planes [0, H)
+        char* hi_ghost = q + (size_t)(s.geo.nzl + kHalo) * 5 * s.geo.plane * bq;
+        Nccl& nc = Nccl::get();
+        timed(2, s, [&] {
+            nc.check(nc.groupStart(), "ncclGroupStart");
+            nc.check(nc.send(top_int, blk, 1, up, comm, s.stream), "ncclSend");
+            nc.check(nc.recv(lo_ghost, blk, 1, dn, comm, s.stream), "ncclRecv");
+            nc.check(nc.send(bot_int, blk, 1, dn, comm, s.stream), "ncclSend");
+            nc.check(nc.recv(hi_ghost, blk, 1, up, comm, s.stream), "ncclRecv");
+            nc.check(nc.groupEnd(), "ncclGroupEnd");
+        });
+        halo_fresh = true;
+        return;
+    }
+    const int ns = (int)slabs.size();
+    if (ns == 1) {
+        Slab& s = slabs[0];
+        CK(cudaSetDevice(s.device));
+        const size_t blk = (size_t)kHalo * 5 * s.geo.plane * bq;
+        char* q = (char*)qcur(s);
+        timed(2, s, [&] {
+            CK(cudaMemcpyAsync(q, q + (size_t)s.geo.nzl * 5 * s.geo.plane * bq, blk,
+                               cudaMemcpyDeviceToDevice, s.stream));
+            CK(cudaMemcpyAsync(q + (size_t)(s.geo.nzl + kHalo) * 5 * s.geo.plane * bq, q + blk, blk,
+                               cudaMemcpyDeviceToDevice, s.stream));
+        });
+        halo_fresh = true;
+        return;
+    }
+    // make every slab's interior visible before cross-slab copies
+    std::vector<cudaEvent_t> ready(ns);
+    for (int i = 0; i < ns; ++i) {
+        CK(cudaSetDevice(slabs[i].device));
+        CK(cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming));
+        CK(cudaEventRecord(ready[i], slabs[i].stream));
+    }
+    for (int i = 0; i < ns; ++i) {
+        Slab& s = slabs[i];
+        const Slab& prv = slabs[(i + ns - 1) % ns];
+        const Slab& nxt = slabs[(i + 1) % ns];
+        CK(cudaSetDevice(s.device));
+        if (ns > 1) {
+            CK(cudaStreamWaitEvent(s.stream, ready[(i + ns - 1) % ns], 0));
+            CK(cudaStreamWaitEvent(s.stream, ready[(i + 1) % ns], 0));
+        }
+        const size_t blk = (size_t)kHalo * 5 * s.geo.plane * bq;
+        char* q = (char*)qcur(s);
+        const char* pq = (const char*)qcur(prv);
+        const char* nq = (const char*)qcur(nxt);
+        timed(2, s, [&] {
+            CK(cudaMemcpyPeerAsync(q, s.device, pq + (size_t)prv.geo.nzl * 5 * prv.geo.plane * bq,
+                                   prv.device, blk, s.stream));
+            CK(cudaMemcpyPeerAsync(q + (size_t)(s.geo.nzl + kHalo) * 5 * s.geo.plane * bq, s.device,
+                                   nq + blk, nxt.device, blk, s.stream));
+        });
+    }
+    // ghost writes must finish before any neighbour overwrites its interior
+    for (int i = 0; i < ns; ++i) {
+        CK(cudaSetDevice(slabs[i].device));
+        CK(cudaEventRecord(ready[i], slabs[i].stream));
+    }
+    for (int i = 0; i < ns && ns > 1; ++i) {
+        CK(cudaSetDevice(slabs[i].device));
+        CK(cudaStreamWaitEvent(slabs[i].stream, ready[(i + ns - 1) % ns], 0));
+        CK(cudaStreamWaitEvent(slabs[i].stream, ready[(i + 1) % ns], 0));
+    }
+    for (int i = 0; i < ns; ++i) cudaEventDestroy(ready[i]);
+    halo_fresh = true;
+}
+
+template <class F>
+void Solver::timed(int cls, const Slab& s, F&& f) {
+    if (!profiling) {
+        f();
+        ++prof_launch[cls];
+        return;
+    }
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, s.stream));
+    f();
+    CK(cudaEventRecord(b, s.stream));
+    prof_ev[cls].push_back({a, b});
+    ++prof_launch[cls];
+}
+
+void Solver::flush_profile() {
+    for (int c = 0; c < 4; ++c) {
+        for (auto& e : prof_ev[c]) {
+            CK(cudaEventSynchronize(e.second));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, e.first, e.second));
+            prof_ms[c] += ms;
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+        prof_ev[c].clear();
+    }
+}
+
+// ResidualEvaluator::evaluate on the staged path (physics.cpp:485-587)
+void Solver::residual_enqueue(int iter, int sub) {
+    if (!halo_fresh) halo_refresh();
+    alloc_staged(*this);
+    const PrimConsts pc = prim_consts();
+    const ResConsts rc = res_consts();
+    const StageConsts sc = stage_consts();
+    const bool staged = strategy == MPFD_DEFAULT && viscous;
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        Slab view = s;
+        view.q = qcur(s);
+        timed(3, s, [&] { launch->prim(view, pc, iter, sub); });
+        if (viscous) timed(3, s, [&] { launch->level2(view, rc, sc, staged); });
+        timed(0, s, [&] { launch->resid(view, rc, iter, sub); });
+        CK(cudaGetLastError());
+    }
+}
+
+void Solver::rk_enqueue(int sub, const double a[3], const double b[3], double dt, int iter) {
+    const RkConsts kc = rk_consts(sub, a, b, dt);
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        Slab view = s;
+        view.q = qcur(s);
+        view.qt = qtcur(s);
+        timed(1, s, [&] { launch->rk(view, kc, iter, sub); });
+        CK(cudaGetLastError());
+    }
+    halo_fresh = false;
+}
+
+// one substep of advance's inner loop: evaluate -> rk_substep -> halo fill
+void Solver::substep_enqueue(int sub, const double a[3], const double b[3], double dt, int iter,
+                             bool write_r) {
+    if (!halo_fresh) halo_refresh();
+    if (use_fused()) {
+        const PrimConsts pc = prim_consts();
+        const ResConsts rc = res_consts();
+        const StageConsts sc = stage_consts();
+        const RkConsts kc = rk_consts(sub, a, b, dt);
+        const bool staged = strategy == MPFD_DEFAULT && viscous;
+        for (auto& s : slabs) {
+            CK(cudaSetDevice(s.device));
+            const void* qin = qbuf ? s.q2 : s.q;
+            void* qout = qbuf ? s.q : s.q2;
+            const void* qtin = qbuf ? s.qt2 : s.qt;
+            void* qtout = qbuf ? s.qt : s.qt2;
+            timed(0, s, [&] {
+                launch->fused(s, qin, qout, qtin, qtout, pc, rc, sc, staged, kc, write_r, iter, sub);
+            });
+            CK(cudaGetLastError());
+        }
+        qbuf ^= 1;
+        halo_fresh = false;
+    } else {
+        residual_enqueue(iter, sub);
+        rk_enqueue(sub, a, b, dt, iter);
+    }
+    halo_refresh();
+}
+
+// true if any slab recorded a divergence (block: synchronous read)
+bool Solver::poll_div(bool block) {
+    int any = 0;
+    for (size_t i = 0; i < slabs.size(); ++i) {
+        Slab& s = slabs[i];
+        CK(cudaSetDevice(s.device));
+        CK(cudaMemcpyAsync(pinned_flag + i, &s.div->flag, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+    }
+    if (!block) {
+        // cheap check: only look if all streams already drained
+        for (auto& s : slabs)
+            if (cudaStreamQuery(s.stream) != cudaSuccess) return false;
+    } else {
+        sync();
+    }
+    for (size_t i = 0; i < slabs.size(); ++i) any |= pinned_flag[i];
+    if (mode == MPFD_DECOMP_NCCL && pz > 1 && block) {
+        int* d = nullptr;
+        Slab& s = slabs[0];
+        CK(cudaMalloc(&d, sizeof(int)));
+        CK(cudaMemcpyAsync(d, &any, sizeof(int), cudaMemcpyHostToDevice, s.stream));
+        Nccl& nc = Nccl::get();
+        nc.check(nc.allReduce(d, d, 1, 2 /*int32*/, 2 /*max*/, comm, s.stream), "ncclAllReduce");
+        CK(cudaMemcpyAsync(&any, d, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+        CK(cudaStreamSynchronize(s.stream));
+        cudaFree(d);
+    }
+    return any != 0;
+}
+
+// reduce the per-slab first-in-scan-order records into one DivergenceEvent
+bool Solver::resolve_div(mpfd_divergence* ev, double dt) {
+    sync();
+    DevDiv tot;
+    std::memset(&tot, 0, sizeof tot);
+    for (auto& row : tot.idx)
+        for (auto& v : row) v = ULLONG_MAX;
+    long long best = LLONG_MAX;
+    for (auto& s : slabs) {
+        DevDiv d;
+        CK(cudaSetDevice(s.device));
+        CK(cudaMemcpy(&d, s.div, sizeof d, cudaMemcpyDeviceToHost));
+        if (!d.flag) continue;
+        tot.flag = 1;
+        const long long key = (long long)d.iter * 3 + d.sub;
+        if (key < best) {
+            best = key;
+            tot.iter = d.iter;
+            tot.sub = d.sub;
+        }
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 5; ++b) tot.idx[a][b] = std::min(tot.idx[a][b], d.idx[a][b]);
+    }
+    if (mode == MPFD_DECOMP_NCCL && pz > 1) {
+        // global min over ranks of (iteration, substep) and the index table
+        unsigned long long buf[16];
+        buf[0] = tot.flag ? (unsigned long long)tot.iter * 3 + tot.sub : ULLONG_MAX;
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 5; ++b) buf[1 + a * 5 + b] = tot.idx[a][b];
+        unsigned long long* d = nullptr;
+        Slab& s = slabs[0];
+        CK(cudaMalloc(&d, sizeof buf));
+        CK(cudaMemcpy(d, buf, sizeof buf, cudaMemcpyHostToDevice));
+        Nccl& nc = Nccl::get();
+        nc.check(nc.allReduce(d, d, 16, 5 /*uint64*/, 3 /*min*/, comm, s.stream), "ncclAllReduce");
+        CK(cudaMemcpy(buf, d, sizeof buf, cudaMemcpyDeviceToHost));
+        cudaFree(d);
+        if (buf[0] == ULLONG_MAX) return false;
+        tot.flag = 1;
+        tot.iter = (int)(buf[0] / 3);
+        tot.sub = (int)(buf[0] % 3);
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 5; ++b) tot.idx[a][b] = buf[1 + a * 5 + b];
+    }
+    if (!tot.flag) return false;
+    // priority of the reference's checks: density (primitives) -> nonfinite
+    // residual -> nonfinite state; components in order, scan order inside
+    for (int code = 0; code < 3; ++code)
+        for (int comp = 0; comp < 5; ++comp) {
+            const unsigned long long gi = tot.idx[code][comp];
+            if (gi == ULLONG_MAX) continue;
+            if (ev) {
+                ev->code = code + 1;
+                ev->i = (int)(gi % (unsigned long long)n);
+                ev->j = (int)((gi / n) % (unsigned long long)n);
+                ev->k = (int)(gi / ((unsigned long long)n * n));
+                ev->iteration = tot.iter;
+                ev->substep = tot.sub;
+                ev->time = code == 2 ? (tot.iter + 1) * dt : tot.iter * dt;
+            }
+            return true;
+        }
+    return false;
+}
+
+// DiagnosticsComputer::compute (tgv.cpp:115-175) with the reference's
+// deterministic_sum tree shape (threads == 1: pure pairwise; > 1: 4096-chunked)
+void Solver::diagnostics(int weighting, double t, int threads, mpfd_diag* out) {
+    if (!halo_fresh) halo_refresh();
+    const size_t N = (size_t)n * n * n;
+    const size_t nch_total = N / 4096;
+    bool aligned = ((size_t)nzl() * n * n) % 4096 == 0 && N >= 4096;
+    if (aligned && threads <= 1 && (nch_total & (nch_total - 1)) != 0) aligned = false;
+    double sums[2];
+    for (int which = 0; which < 2; ++which) {
+        std::vector<double> parts;  // global-order chunk sums, or the full integrand
+        for (auto& s : slabs) {
+            CK(cudaSetDevice(s.device));
+            Slab view = s;
+            view.q = qcur(s);
+            launch->diag_integrand(view, which, weighting, 1.0 / (12.0 * h));
+            CK(cudaGetLastError());
+            const size_t nint = (size_t)s.geo.nzl * s.geo.plane;
+            if (aligned) {
+                const long long nch = (long long)(nint / 4096);
+                k_chunk_sums<<<(unsigned)((nch * 32 + 255) / 256), 256, 0, s.stream>>>(s.diag, nch, s.partials);
+                CK(cudaGetLastError());
+                const size_t o = parts.size();
+                parts.resize(o + nch);
+                CK(cudaMemcpyAsync(parts.data() + o, s.partials, nch * sizeof(double), cudaMemcpyDeviceToHost,
+                                   s.stream));
+            } else {
+                const size_t o = parts.size();
+                parts.resize(o + nint);
+                CK(cudaMemcpyAsync(parts.data() + o, s.diag, nint * sizeof(double), cudaMemcpyDeviceToHost,
+                                   s.stream));
+            }
+            CK(cudaStreamSynchronize(s.stream));
+        }
+        if (mode == MPFD_DECOMP_NCCL && pz > 1) {
+            // gather every rank's parts in rank (= global z) order
+            Slab& s = slabs[0];
+            const size_t cnt = parts.size();
+            double* d = nullptr;
+            CK(cudaMalloc(&d, cnt * pz * sizeof(double)));
+            CK(cudaMemcpy(d + cnt * rank, parts.data(), cnt * sizeof(double), cudaMemcpyHostToDevice));
+            Nccl& nc = Nccl::get();
+            nc.check(nc.allGather(d + cnt * rank, d, cnt, 8 /*float64*/, comm, s.stream), "ncclAllGather");
+            parts.resize(cnt * pz);
+            CK(cudaMemcpyAsync(parts.data(), d, cnt * pz * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+            CK(cudaStreamSynchronize(s.stream));
+            cudaFree(d);
+        }
+        double sum;
+        if (aligned) {
+            const size_t nch = parts.size();
+            const bool pow2 = (nch & (nch - 1)) == 0;
+            if (N <= 4096) sum = parts[0];
+            else if (threads > 1) sum = pairwise_sum(parts.data(), nch);
+            else sum = tree_of_chunks(parts.data(), nch);  // nch is a power of two here
+            (void)pow2;
+        } else {
+            if (threads > 1 && N > 4096) {
+                const size_t nch = (N + 4095) / 4096;
+                std::vector<double> c(nch);
+                for (size_t i = 0; i < nch; ++i) c[i] = pairwise_sum(parts.data() + i * 4096, std::min<size_t>(4096, N - i * 4096));
+                sum = pairwise_sum(c.data(), nch);
+            } else {
+                sum = pairwise_sum(parts.data(), N);
+            }
+        }
+        sums[which] = sum;
+    }
+    const double cell = h * h * h;
+    const double vol = L * L * L;
+    out->t = t;
+    out->kinetic_energy = sums[0] * cell / vol;
+    out->enstrophy = sums[1] * cell / vol;
+    out->eps_s = re > 0.0 ? out->enstrophy / re : 0.0;
+    out->ke_normalized = 0.0;
+    out->diverged = 0;
+}
+
+}  // namespace mpfd_b200
+
+// ===========================================================================
+// C-ABI
+using namespace mpfd_b200;
+
+struct mpfd_solver {
+    Solver s;
+};
+
+template <class F>
+static int guard(F&& f) {
+    try {
+        return f();
+    } catch (const ConfigError& e) {
+        g_err = e.what();
+        return MPFD_ECONFIG;
+    } catch (const DeviceError& e) {
+        g_err = e.what();
+        return MPFD_EDEVICE;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return MPFD_EDEVICE;
+    }
+}
+
+extern "C" {
+
+const char* mpfd_b200_last_error(void) { return g_err.c_str(); }
+const char* mpfd_b200_version(void) { return "mpfd_b200 0.1 (sm_100a)"; }
+
+int mpfd_b200_resolve_preset(const char* name, mpfd_precision* out) {
+    return guard([&] {
+        Precision p;
+        if (!name || !preset(name, p)) throw ConfigError(std::string("unknown precision preset '") + (name ? name : "") + "'");
+        std::memset(out, 0, sizeof *out);
+        out->q_vector = p.q;
+        out->rk_arrays = p.rk;
+        out->residuals = p.res;
+        out->wk_arrays = p.wk;
+        out->emulation = MPFD_STRICT;
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_split_preset(const char* name, mpfd_split* out) {
+    return guard([&] {
+        double w[7];
+        if (!name || !split(name, w)) throw ConfigError(std::string("unknown split form '") + (name ? name : "") + "'");
+        *out = {w[0], w[1], w[2], w[3], w[4], w[5], w[6]};
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_nccl_unique_id(void* out128) {
+    return guard([&] {
+        Nccl& nc = Nccl::get();
+        nc.check(nc.getUniqueId(out128), "ncclGetUniqueId");
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_create(const mpfd_grid* grid, const mpfd_precision* prec, int strategy, const mpfd_flow* flow,
+                     const mpfd_split* split_, const mpfd_decomp* decomp, mpfd_solver** out) {
+    return guard([&] {
+        if (!out) throw ConfigError("null output pointer");
+        *out = nullptr;
+        auto h = std::make_unique<mpfd_solver>();
+        h->s.setup(grid, prec, strategy, flow, split_, decomp);
+        *out = h.release();
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_destroy(mpfd_solver* s) {
+    return guard([&] {
+        delete s;
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_init_tgv(mpfd_solver* s) {
+    return guard([&] {
+        s->s.init(0);
+        return MPFD_OK;
+    });
+}
+int mpfd_b200_init_uniform(mpfd_solver* s) {
+    return guard([&] {
+        s->s.init(1);
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_set_state(mpfd_solver* s, int cls, int comp, const double* ext3) {
+    return guard([&] {
+        const size_t e = (size_t)s->s.n + 8;
+        s->s.set_interior(cls, comp, ext3, e, e * e, (int)((4 * e + 4) * e + 4));
+        s->s.reset_div();
+        return MPFD_OK;
+    });
+}
+int mpfd_b200_get_state(mpfd_solver* s, int cls, int comp, double* ext3) {
+    return guard([&] {
+        const int n = s->s.n;
+        const size_t e = (size_t)n + 8;
+        s->s.get_interior(cls, comp, ext3, e, e * e, (int)((4 * e + 4) * e + 4));
+        // periodic halos (fill_halos_periodic, field.cpp:9-48) for Q; the
+        // reference never fills Qt/R halos, which stay zero
+        if (cls == 0) {
+            for (size_t kk = 4; kk < (size_t)n + 4; ++kk)
+                for (size_t jj = 4; jj < (size_t)n + 4; ++jj) {
+                    double* row = ext3 + (kk * e + jj) * e;
+                    for (int hh = 0; hh < 4; ++hh) {
+                        row[hh] = row[hh + n];
+                        row[4 + n + hh] = row[4 + hh];
+                    }
+                }
+            for (size_t kk = 4; kk < (size_t)n + 4; ++kk) {
+                double* pl = ext3 + kk * e * e;
+                for (int hh = 0; hh < 4; ++hh) {
+                    std::memcpy(pl + hh * e, pl + (hh + n) * e, e * sizeof(double));
+                    std::memcpy(pl + (4 + n + hh) * e, pl + (4 + hh) * e, e * sizeof(double));
+                }
+            }
+            for (int hh = 0; hh < 4; ++hh) {
+                std::memcpy(ext3 + hh * e * e, ext3 + (hh + n) * e * e, e * e * sizeof(double));
+                std::memcpy(ext3 + (4 + n + hh) * e * e, ext3 + (4 + hh) * e * e, e * e * sizeof(double));
+            }
+        }
+        return MPFD_OK;
+    });
+}
+int mpfd_b200_set_state_interior(mpfd_solver* s, int cls, int comp, const double* n3) {
+    return guard([&] {
+        const size_t n = (size_t)s->s.n;
+        s->s.set_interior(cls, comp, n3, n, n * n, 0);
+        s->s.reset_div();
+        return MPFD_OK;
+    });
+}
+int mpfd_b200_get_state_interior(mpfd_solver* s, int cls, int comp, double* n3) {
+    return guard([&] {
+        const size_t n = (size_t)s->s.n;
+        s->s.get_interior(cls, comp, n3, n, n * n, 0);
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_residual(mpfd_solver* h, mpfd_divergence* ev) {
+    return guard([&] {
+        Solver& S = h->s;
+        S.reset_div();
+        S.residual_enqueue(0, 0);
+        S.sync();
+        mpfd_divergence e{};
+        if (S.resolve_div(&e, 0.0)) {
+            e.time = -1.0;
+            e.iteration = -1;
+            e.substep = -1;
+            if (ev) *ev = e;
+            S.reset_div();
+            return MPFD_DIVERGED;
+        }
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_rk_substep(mpfd_solver* h, int substep, const double a[3], const double b[3], double dt,
+                         mpfd_divergence* ev) {
+    return guard([&] {
+        Solver& S = h->s;
+        if (substep < 0 || substep > 2) throw ConfigError("substep out of range");
+        S.reset_div();
+        S.rk_enqueue(substep, a, b, dt, 0);
+        S.sync();
+        mpfd_divergence e{};
+        if (S.resolve_div(&e, dt)) {
+            if (ev) *ev = e;
+            S.reset_div();
+            return MPFD_DIVERGED;
+        }
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_halo_refresh(mpfd_solver* h) {
+    return guard([&] {
+        h->s.halo_refresh();
+        h->s.sync();
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_diagnostics(mpfd_solver* h, int weighting, double t, int threads, mpfd_diag* out) {
+    return guard([&] {
+        h->s.diagnostics(weighting, t, threads, out);
+        return MPFD_OK;
+    });
+}
+
+static void check_step(const mpfd_step* st) {
+    if (!st) throw ConfigError("null step");
+    if (!(st->dt > 0)) throw ConfigError("dt must be positive");
+}
+
+int mpfd_b200_advance(mpfd_solver* h, const mpfd_step* st, mpfd_diag* series, long cap, long* len,
+                      mpfd_divergence* ev, long* iters) {
+    return guard([&] {
+        check_step(st);
+        Solver& S = h->s;
+        long count = 0;
+        double k0 = 0.0;
+        auto sample = [&](double t, bool diverged) {
+            if (!series || count >= cap) return;
+            mpfd_diag d;
+            S.diagnostics(st->ke_weighting, t, st->threads, &d);
+            d.diverged = diverged ? 1 : 0;
+            if (count == 0) k0 = d.kinetic_energy;
+            d.ke_normalized = k0 != 0.0 ? d.kinetic_energy / k0 : 0.0;
+            series[count++] = d;
+        };
+        S.reset_div();
+        S.halo_refresh();
+        sample(0.0, false);
+        const int qbuf_start = S.qbuf;
+        long done = 0;
+        int status = MPFD_OK;
+        mpfd_divergence e{};
+        const bool multi = S.mode == MPFD_DECOMP_NCCL && S.pz > 1;
+        for (long it = 0; it < st->n_iterations; ++it) {
+            const bool last = it + 1 == st->n_iterations;
+            for (int sub = 0; sub < 3; ++sub)
+                S.substep_enqueue(sub, st->a, st->b, st->dt, (int)it, last && sub == 2);
+            const bool due = st->diagnostics_interval > 0 && (it + 1) % st->diagnostics_interval == 0;
+            const bool check = due || last || (!multi && (it % 8) == 7) || (multi && (it % 64) == 63);
+            if (check && S.poll_div(true)) {
+                S.resolve_div(&e, st->dt);
+                status = MPFD_DIVERGED;
+                done = e.iteration;
+                // the fused path double-buffers Q and Qt: the state the reference
+                // holds at the event is the input of the failing substep (density /
+                // residual signal) or its output (nonfinite state); every launched
+                // substep flipped the buffer index, no-op launches included
+                if (S.use_fused()) {
+                    const long failed = e.iteration * 3 + e.substep;
+                    const long keep = e.code == 3 ? failed + 1 : failed;
+                    S.qbuf = qbuf_start ^ (int)(keep & 1);
+                    if (e.code == 2) {
+                        // R as the reference leaves it: the nonfinite residual
+                        S.reset_div();
+                        S.halo_fresh = false;
+                        S.residual_enqueue((int)e.iteration, e.substep);
+                        S.sync();
+                    }
+                }
+                S.halo_fresh = false;
+                sample(e.time, true);
+                break;
+            }
+            done = it + 1;
+            if (due) sample((it + 1) * st->dt, false);
+        }
+        S.sync();
+        if (len) *len = count;
+        if (iters) *iters = done;
+        if (ev) *ev = e;
+        return status;
+    });
+}
+
+void* mpfd_b200_stream(mpfd_solver* h) { return h ? (void*)h->s.slabs[0].stream : nullptr; }
+
+int mpfd_b200_synchronize(mpfd_solver* h) {
+    return guard([&] {
+        h->s.sync();
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_run_steps(mpfd_solver* h, const mpfd_step* st, long iters) {
+    return guard([&] {
+        check_step(st);
+        Solver& S = h->s;
+        for (long it = 0; it < iters; ++it)
+            for (int sub = 0; sub < 3; ++sub) S.substep_enqueue(sub, st->a, st->b, st->dt, (int)it, false);
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_profile(mpfd_solver* h, int enable) {
+    return guard([&] {
+        Solver& S = h->s;
+        S.flush_profile();
+        S.profiling = enable != 0;
+        for (int c = 0; c < 4; ++c) {
+            S.prof_ms[c] = 0;
+            S.prof_launch[c] = 0;
+        }
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_profile_read(mpfd_solver* h, double ms[4], long launches[4]) {
+    return guard([&] {
+        Solver& S = h->s;
+        S.flush_profile();
+        for (int c = 0; c < 4; ++c) {
+            ms[c] = S.prof_ms[c];
+            launches[c] = S.prof_launch[c];
+        }
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_memory(mpfd_solver* h, size_t* device_bytes, size_t* census, size_t* census_b64) {
+    return guard([&] {
+        Solver& S = h->s;
+        size_t b = 0;
+        for (auto& s : S.slabs) b += s.bytes;
+        if (device_bytes) *device_bytes = b;
+        // memory_report over make_solver_fields' set (registry.cpp:24-39)
+        const size_t e = (size_t)S.n + 8;
+        const size_t pts = e * e * e;
+        size_t tot = 0, cnt = 0;
+        for (int c = 0; c < 5; ++c) {
+            tot += pts * byte_width(S.prec.resolve(0, kQNames[c]));
+            tot += pts * byte_width(S.prec.resolve(1, kTNames[c]));
+            tot += pts * byte_width(S.prec.resolve(2, kRNames[c]));
+            tot += pts * byte_width(S.prec.resolve(3, kPNames[c]));
+            cnt += 4;
+        }
+        if (S.strategy == MPFD_DEFAULT)
+            for (int i = 0; i < 12; ++i) {
+                tot += pts * byte_width(S.prec.resolve(3, kGNames[i]));
+                ++cnt;
+            }
+        if (census) *census = tot;
+        if (census_b64) *census_b64 = cnt * pts * 8;
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_set_path(mpfd_solver* h, int path) {
+    return guard([&] {
+        Solver& S = h->s;
+        if (path == 1 && !S.launch->fused_available()) throw ConfigError("fused path not available for this precision plan");
+        if (path != S.path) {
+            // move the state into the primary buffers before switching
+            if (S.path == 1 && S.qbuf) {
+                for (auto& s : S.slabs) {
+                    CK(cudaSetDevice(s.device));
+                    const size_t qel = (size_t)s.geo.planes * 5 * s.geo.plane * byte_width(S.plan.qk);
+                    const size_t tel = (size_t)s.geo.nzl * 5 * s.geo.plane * byte_width(S.plan.tk);
+                    CK(cudaMemcpyAsync(s.q, s.q2, qel, cudaMemcpyDeviceToDevice, s.stream));
+                    CK(cudaMemcpyAsync(s.qt, s.qt2, tel, cudaMemcpyDeviceToDevice, s.stream));
+                }
+                S.qbuf = 0;
+            }
+            S.path = path;
+        }
+        S.sync();
+        return MPFD_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,439 @@
+"""Python mirror of the reference solver API over the B200 C-ABI.
+
+Reference names kept (file:line in /root/reference/proj):
+  PrecisionConfig / resolve_preset     precision.hpp:181-199, precision.cpp:58-88
+  GridSpec                             field.hpp:20-56
+  FlowParams                           physics.hpp:26-34
+  SplitCoefficients / split_preset     physics.hpp:40-63, physics.cpp:19-43
+  RKScheme / StepConfig                integrate.hpp:18-28
+  DivergenceEvent                      physics.hpp:85-91
+  DiagnosticsRecord                    tgv.hpp:13-20
+  AdvanceResult                        integrate.hpp:35-43
+  Solver = make_solver_fields + ResidualEvaluator + rk_substep + advance +
+           DiagnosticsComputer         physics.cpp:441-587, integrate.cpp:47-167,
+                                       tgv.cpp:29-175
+Errors mirror the reference: ConfigError for configuration problems,
+divergence reported as a value (DivergenceEvent), DeviceError for CUDA/NCCL.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+library_path = os.path.join(HERE, "libmpfd_b200.so")
+
+B16, B32, B64 = 0, 1, 2
+STRICT, STOREROUND = 0, 1
+DEFAULT, STORESOME = 0, 1
+_KIND = {"B16": B16, "B32": B32, "B64": B64}
+
+
+class ConfigError(ValueError):
+    """ConfigError / RegistryError (precision.hpp:23-28)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA or NCCL failure inside the B200 library."""
+
+
+# ---------------------------------------------------------------------------
+# C structs (include/mpfd_b200.h)
+class _Grid(C.Structure):
+    _fields_ = [("n", C.c_int), ("domain_length", C.c_double)]
+
+
+class _Prec(C.Structure):
+    _fields_ = [("q_vector", C.c_int), ("rk_arrays", C.c_int), ("residuals", C.c_int),
+                ("wk_arrays", C.c_int), ("emulation", C.c_int), ("n_overrides", C.c_int),
+                ("override_names", C.POINTER(C.c_char_p)), ("override_kinds", C.POINTER(C.c_int))]
+
+
+class _Flow(C.Structure):
+    _fields_ = [("mach", C.c_double), ("reynolds", C.c_double), ("prandtl", C.c_double),
+                ("gamma", C.c_double), ("viscous", C.c_int)]
+
+
+class _Split(C.Structure):
+    _fields_ = [(k, C.c_double) for k in
+                ("alpha", "beta_rho", "beta_u", "beta_phi", "gamma_rho", "gamma_u", "gamma_phi")]
+
+
+class _Decomp(C.Structure):
+    _fields_ = [("pz", C.c_int), ("mode", C.c_int), ("rank", C.c_int), ("device", C.c_int),
+                ("devices", C.POINTER(C.c_int)), ("nccl_id", C.c_void_p)]
+
+
+class _Div(C.Structure):
+    _fields_ = [("code", C.c_int), ("i", C.c_int), ("j", C.c_int), ("k", C.c_int),
+                ("time", C.c_double), ("iteration", C.c_long), ("substep", C.c_int)]
+
+
+class _Diag(C.Structure):
+    _fields_ = [("t", C.c_double), ("kinetic_energy", C.c_double), ("enstrophy", C.c_double),
+                ("eps_s", C.c_double), ("ke_normalized", C.c_double), ("diverged", C.c_int)]
+
+
+class _Step(C.Structure):
+    _fields_ = [("a", C.c_double * 3), ("b", C.c_double * 3), ("dt", C.c_double),
+                ("n_iterations", C.c_long), ("diagnostics_interval", C.c_int),
+                ("ke_weighting", C.c_int), ("threads", C.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    """The loaded C-ABI library.  Raises if the sm_100a extension is missing:
+    the product path has no CPU fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(library_path):
+            raise ImportError(
+                f"{library_path} is missing: build it with `python -m "
+                "paper_2505_20911_b200.build` (nvcc, sm_100a)")
+        L = C.CDLL(library_path)
+        P = C.c_void_p
+        I = C.c_int
+        D = C.c_double
+        L.mpfd_b200_last_error.restype = C.c_char_p
+        L.mpfd_b200_version.restype = C.c_char_p
+        L.mpfd_b200_resolve_preset.argtypes = [C.c_char_p, C.POINTER(_Prec)]
+        L.mpfd_b200_split_preset.argtypes = [C.c_char_p, C.POINTER(_Split)]
+        L.mpfd_b200_nccl_unique_id.argtypes = [P]
+        L.mpfd_b200_create.argtypes = [C.POINTER(_Grid), C.POINTER(_Prec), I, C.POINTER(_Flow),
+                                       C.POINTER(_Split), C.POINTER(_Decomp), C.POINTER(P)]
+        L.mpfd_b200_destroy.argtypes = [P]
+        L.mpfd_b200_init_tgv.argtypes = [P]
+        L.mpfd_b200_init_uniform.argtypes = [P]
+        DP = C.POINTER(D)
+        for fn in ("set_state", "get_state", "set_state_interior", "get_state_interior"):
+            getattr(L, "mpfd_b200_" + fn).argtypes = [P, I, I, DP]
+        L.mpfd_b200_residual.argtypes = [P, C.POINTER(_Div)]
+        L.mpfd_b200_rk_substep.argtypes = [P, I, DP, DP, D, C.POINTER(_Div)]
+        L.mpfd_b200_halo_refresh.argtypes = [P]
+        L.mpfd_b200_diagnostics.argtypes = [P, I, D, I, C.POINTER(_Diag)]
+        L.mpfd_b200_advance.argtypes = [P, C.POINTER(_Step), C.POINTER(_Diag), C.c_long,
+                                        C.POINTER(C.c_long), C.POINTER(_Div), C.POINTER(C.c_long)]
+        L.mpfd_b200_stream.restype = P
+        L.mpfd_b200_stream.argtypes = [P]
+        L.mpfd_b200_synchronize.argtypes = [P]
+        L.mpfd_b200_run_steps.argtypes = [P, C.POINTER(_Step), C.c_long]
+        L.mpfd_b200_profile.argtypes = [P, I]
+        L.mpfd_b200_profile_read.argtypes = [P, DP, C.POINTER(C.c_long)]
+        L.mpfd_b200_memory.argtypes = [P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
+                                       C.POINTER(C.c_size_t)]
+        L.mpfd_b200_set_path.argtypes = [P, I]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc == 0 or rc == 2:
+        return rc
+    msg = lib().mpfd_b200_last_error().decode()
+    if rc == 1:
+        raise ConfigError(msg)
+    raise DeviceError(msg)
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class PrecisionConfig:
+    q_vector: int = B64
+    rk_arrays: int = B64
+    residuals: int = B64
+    wk_arrays: int = B64
+    custom_overrides: Dict[str, int] = field(default_factory=dict)
+    emulation: int = STRICT
+
+    def resolve(self, cls: int, name: str) -> int:
+        if name in self.custom_overrides:
+            return self.custom_overrides[name]
+        if cls == 4:
+            return B64
+        return (self.q_vector, self.rk_arrays, self.residuals, self.wk_arrays)[cls]
+
+
+def resolve_preset(name: str, emulation: str | int = STRICT) -> PrecisionConfig:
+    p = _Prec()
+    _check(lib().mpfd_b200_resolve_preset(name.encode(), C.byref(p)))
+    emu = emulation if isinstance(emulation, int) else (
+        STRICT if emulation == "strict" else STOREROUND)
+    return PrecisionConfig(p.q_vector, p.rk_arrays, p.residuals, p.wk_arrays, {}, emu)
+
+
+@dataclass
+class GridSpec:
+    n: int = 32
+    domain_length: float = 2.0 * math.pi
+
+    halo_depth = 4
+
+    def __post_init__(self):
+        if self.n < 5:
+            raise ConfigError("GridSpec: n must be >= 5")
+
+    def spacing(self) -> float:
+        return self.domain_length / self.n
+
+    def ext(self) -> int:
+        return self.n + 2 * self.halo_depth
+
+
+@dataclass
+class FlowParams:
+    mach: float = 0.5
+    reynolds: float = 800.0
+    prandtl: float = 0.72
+    gamma: float = 1.4
+    viscous: bool = True
+
+
+@dataclass
+class SplitCoefficients:
+    alpha: float = 1.0
+    beta_rho: float = 0.0
+    beta_u: float = 0.0
+    beta_phi: float = 0.0
+    gamma_rho: float = 0.0
+    gamma_u: float = 0.0
+    gamma_phi: float = 0.0
+
+
+def split_preset(name: str) -> SplitCoefficients:
+    s = _Split()
+    _check(lib().mpfd_b200_split_preset(name.encode(), C.byref(s)))
+    return SplitCoefficients(*(getattr(s, k) for k, _ in _Split._fields_))
+
+
+@dataclass
+class RKScheme:
+    a: Tuple[float, float, float] = (0.0, -5.0 / 9.0, -153.0 / 128.0)
+    b: Tuple[float, float, float] = (1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0)
+
+
+@dataclass
+class StepConfig:
+    dt: float = 0.005
+    n_iterations: int = 4000
+    diagnostics_interval: int = 100
+
+
+@dataclass
+class DivergenceEvent:
+    what: str
+    i: int
+    j: int
+    k: int
+    time: float = -1.0
+    iteration: int = -1
+    substep: int = -1
+
+
+_WHAT = {1: "nonpositive or nonfinite density", 2: "nonfinite residual", 3: "nonfinite state"}
+
+
+@dataclass
+class DiagnosticsRecord:
+    t: float = 0.0
+    kinetic_energy: float = 0.0
+    enstrophy: float = 0.0
+    eps_s: float = 0.0
+    ke_normalized: float = 0.0
+    diverged: bool = False
+
+
+@dataclass
+class AdvanceResult:
+    diverged: bool
+    divergence: Optional[DivergenceEvent]
+    iterations_run: int
+    series: List[DiagnosticsRecord]
+
+
+@dataclass
+class Decomposition:
+    """z-slab decomposition: pz slabs, LOCAL (all slabs in this process) or
+    NCCL (one slab per rank, `nccl_id` from Solver.nccl_unique_id())."""
+    pz: int = 1
+    mode: int = 0
+    rank: int = 0
+    device: int = 0
+    devices: Optional[List[int]] = None
+    nccl_id: Optional[bytes] = None
+
+
+def _div(d: _Div) -> DivergenceEvent:
+    return DivergenceEvent(_WHAT.get(d.code, "?"), d.i, d.j, d.k, d.time, d.iteration, d.substep)
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class Solver:
+    """make_solver_fields + ResidualEvaluator + the RK driver on B200."""
+
+    def __init__(self, grid: GridSpec, precision: PrecisionConfig, strategy: int | str,
+                 flow: FlowParams, split: SplitCoefficients | str = "Blaisdell",
+                 decomp: Optional[Decomposition] = None):
+        L = lib()
+        if isinstance(strategy, str):
+            if strategy not in ("default", "storesome"):
+                raise ConfigError(f"unknown strategy '{strategy}' (expected default or storesome)")
+            strategy = DEFAULT if strategy == "default" else STORESOME
+        if isinstance(split, str):
+            split = split_preset(split)
+        self.grid, self.precision, self.flow, self.split = grid, precision, flow, split
+        self.n = grid.n
+        names = list(precision.custom_overrides)
+        self._keep = [n.encode() for n in names]
+        p = _Prec(precision.q_vector, precision.rk_arrays, precision.residuals,
+                  precision.wk_arrays, precision.emulation, len(names),
+                  (C.c_char_p * max(1, len(names)))(*self._keep),
+                  (C.c_int * max(1, len(names)))(*[precision.custom_overrides[k] for k in names]))
+        g = _Grid(grid.n, grid.domain_length)
+        f = _Flow(flow.mach, flow.reynolds, flow.prandtl, flow.gamma, 1 if flow.viscous else 0)
+        s = _Split(*(getattr(split, k) for k, _ in _Split._fields_))
+        d = decomp or Decomposition()
+        self._devs = (C.c_int * max(1, len(d.devices or [])))(*(d.devices or [0]))
+        self._nid = C.create_string_buffer(d.nccl_id, 128) if d.nccl_id else None
+        dd = _Decomp(d.pz, d.mode, d.rank, d.device,
+                     self._devs if d.devices else None,
+                     C.cast(self._nid, C.c_void_p) if self._nid else None)
+        self.h = C.c_void_p()
+        _check(L.mpfd_b200_create(C.byref(g), C.byref(p), strategy, C.byref(f), C.byref(s),
+                                  C.byref(dd), C.byref(self.h)))
+        self.L = L
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            self.L.mpfd_b200_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().mpfd_b200_nccl_unique_id(buf))
+        return buf.raw
+
+    # --- setup ------------------------------------------------------------
+    def init_tgv(self):
+        _check(self.L.mpfd_b200_init_tgv(self.h))
+
+    def init_uniform(self):
+        _check(self.L.mpfd_b200_init_uniform(self.h))
+
+    # --- carriers ----------------------------------------------------------
+    def get_field(self, cls: int, comp: int) -> np.ndarray:
+        """Interior n^3 binary64 carrier, indexed [k, j, i]."""
+        out = np.empty((self.n,) * 3)
+        _check(self.L.mpfd_b200_get_state_interior(self.h, cls, comp, _dp(out)))
+        return out
+
+    def set_field(self, cls: int, comp: int, arr: np.ndarray):
+        a = np.ascontiguousarray(arr, dtype=np.float64)
+        _check(self.L.mpfd_b200_set_state_interior(self.h, cls, comp, _dp(a)))
+
+    def get_state(self, cls: int) -> np.ndarray:
+        return np.stack([self.get_field(cls, c) for c in range(5)])
+
+    def set_state(self, cls: int, arr: np.ndarray):
+        for c in range(5):
+            self.set_field(cls, c, arr[c])
+
+    def get_field_ext(self, cls: int, comp: int) -> np.ndarray:
+        e = self.n + 8
+        out = np.zeros((e, e, e))
+        _check(self.L.mpfd_b200_get_state(self.h, cls, comp, _dp(out)))
+        return out
+
+    def set_field_ext(self, cls: int, comp: int, arr: np.ndarray):
+        a = np.ascontiguousarray(arr, dtype=np.float64)
+        _check(self.L.mpfd_b200_set_state(self.h, cls, comp, _dp(a)))
+
+    # --- hot path ----------------------------------------------------------
+    def evaluate(self) -> Optional[DivergenceEvent]:
+        """ResidualEvaluator::evaluate (physics.cpp:485-587)."""
+        d = _Div()
+        rc = _check(self.L.mpfd_b200_residual(self.h, C.byref(d)))
+        return _div(d) if rc == 2 else None
+
+    def rk_substep(self, substep: int, dt: float, scheme: RKScheme = RKScheme()
+                   ) -> Optional[DivergenceEvent]:
+        """rk_substep (integrate.cpp:47-91) + advance's finite guard."""
+        a = np.array(scheme.a, dtype=np.float64)
+        b = np.array(scheme.b, dtype=np.float64)
+        d = _Div()
+        rc = _check(self.L.mpfd_b200_rk_substep(self.h, substep, _dp(a), _dp(b), dt, C.byref(d)))
+        return _div(d) if rc == 2 else None
+
+    def fill_state_halos(self):
+        _check(self.L.mpfd_b200_halo_refresh(self.h))
+
+    def diagnostics(self, weighting: int = 0, t: float = 0.0, threads: int = 8
+                    ) -> DiagnosticsRecord:
+        d = _Diag()
+        _check(self.L.mpfd_b200_diagnostics(self.h, weighting, t, threads, C.byref(d)))
+        return DiagnosticsRecord(d.t, d.kinetic_energy, d.enstrophy, d.eps_s, d.ke_normalized,
+                                 bool(d.diverged))
+
+    def _step(self, step: StepConfig, scheme: RKScheme, weighting: int, threads: int) -> _Step:
+        return _Step((C.c_double * 3)(*scheme.a), (C.c_double * 3)(*scheme.b), step.dt,
+                     step.n_iterations, step.diagnostics_interval, weighting, threads)
+
+    def advance(self, step: StepConfig, scheme: RKScheme = RKScheme(), weighting: int = 0,
+                threads: int = 8, cap: int = 100000) -> AdvanceResult:
+        """advance (integrate.cpp:97-167) with diagnostics sampling."""
+        st = self._step(step, scheme, weighting, threads)
+        cap = min(cap, 2 + (step.n_iterations // max(1, step.diagnostics_interval)
+                            if step.diagnostics_interval > 0 else 0) + 2)
+        series = (_Diag * cap)()
+        ln, it = C.c_long(0), C.c_long(0)
+        d = _Div()
+        rc = _check(self.L.mpfd_b200_advance(self.h, C.byref(st), series, cap, C.byref(ln),
+                                             C.byref(d), C.byref(it)))
+        recs = [DiagnosticsRecord(x.t, x.kinetic_energy, x.enstrophy, x.eps_s, x.ke_normalized,
+                                  bool(x.diverged)) for x in series[: ln.value]]
+        return AdvanceResult(rc == 2, _div(d) if rc == 2 else None, it.value, recs)
+
+    # --- measurement hooks --------------------------------------------------
+    def run_steps(self, iters: int, dt: float, scheme: RKScheme = RKScheme()):
+        st = self._step(StepConfig(dt, iters, 0), scheme, 0, 8)
+        _check(self.L.mpfd_b200_run_steps(self.h, C.byref(st), iters))
+
+    def synchronize(self):
+        _check(self.L.mpfd_b200_synchronize(self.h))
+
+    @property
+    def stream(self) -> int:
+        return self.L.mpfd_b200_stream(self.h) or 0
+
+    def profile(self, enable: bool):
+        _check(self.L.mpfd_b200_profile(self.h, 1 if enable else 0))
+
+    def profile_read(self):
+        ms = np.zeros(4)
+        ln = (C.c_long * 4)()
+        _check(self.L.mpfd_b200_profile_read(self.h, _dp(ms), ln))
+        return ms, list(ln)
+
+    def memory(self):
+        a, b, c = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        _check(self.L.mpfd_b200_memory(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def set_path(self, path: str):
+        _check(self.L.mpfd_b200_set_path(self.h, 1 if path == "fused" else 0))

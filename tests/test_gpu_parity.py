@@ -1,0 +1,219 @@
+"""GPU parity: the B200 solver against the reference itself (oracle/_ref) and
+the C restatement (oracle/), bit for bit.
+
+Contract (parity build): Q, Qt and R are *bitwise*
+equal to the reference after every substep, for every preset x emulation x
+strategy; diagnostics agree bitwise on bitwise-equal states (same reduction
+tree).  Checkers are run on the same seeded/deterministic inputs.
+"""
+import numpy as np
+import pytest
+
+import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+PRESETS = list(po.PRESETS)
+EMUL = ["strict", "storeround"]
+STRATS = ["default", "storesome"]
+
+
+def checker(n, **kw):
+    """The reference library when present, else the (reference-pinned) oracle."""
+    if po.ref_available():
+        return po.Reference(n, **kw)
+    kw.pop("threads", None)
+    return po.Oracle(n, **kw)
+
+
+def b200_solver(m, n, preset="DP", emulation="strict", strategy="storesome", split="Blaisdell",
+                mach=0.1, re=1600.0, pr=0.72, gamma=1.4, viscous=True, overrides=None,
+                decomp=None, path=None):
+    prec = m.resolve_preset(preset, emulation)
+    if overrides:
+        prec.custom_overrides = {k: po.KIND_NAMES[v] for k, v in overrides.items()}
+    s = m.Solver(m.GridSpec(n), prec, strategy, m.FlowParams(mach, re, pr, gamma, viscous), split,
+                 decomp)
+    if path:
+        s.set_path(path)
+    return s
+
+
+def same_bits(a, b):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    return np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def assert_state(s, c, classes=(0, 1, 2), ctx=""):
+    for cls in classes:
+        for comp in range(5):
+            g, r = s.get_field(cls, comp), c.field(cls, comp)
+            if not same_bits(g, r):
+                bad = np.argwhere(g.view(np.uint64) != r.view(np.uint64))
+                k, j, i = bad[0]
+                raise AssertionError(
+                    f"{ctx} class {cls} comp {comp}: {len(bad)} mismatches, first (i,j,k)=({i},{j},{k})"
+                    f" gpu={g[k, j, i]!r} ref={r[k, j, i]!r}")
+
+
+def test_double_rounding_kat(b200):
+    """Stores round once from binary64 (test_precision.cpp:141-146)."""
+    s = b200_solver(b200, 8, "HP")
+    x = 1.0 + 2.0**-11 + 2.0**-40
+    s.set_field(0, 0, np.full((8, 8, 8), x))
+    assert s.get_field(0, 0)[0, 0, 0] == 1.0 + 2.0**-10
+    s.set_field(0, 0, np.full((8, 8, 8), 65520.0))
+    assert np.isinf(s.get_field(0, 0)[0, 0, 0])
+    s.set_field(0, 0, np.full((8, 8, 8), 2.0**-25))
+    assert s.get_field(0, 0)[0, 0, 0] == 0.0
+
+
+@pytest.mark.parametrize("preset", PRESETS)
+def test_init_tgv(b200, preset):
+    s = b200_solver(b200, 16, preset)
+    s.init_tgv()
+    c = checker(16, preset=preset)
+    c.init()
+    assert_state(s, c, (0, 1, 2), f"init {preset}")
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("emulation", EMUL)
+@pytest.mark.parametrize("preset", PRESETS)
+def test_substeps_bitwise(b200, preset, emulation, strategy):
+    """evaluate -> rk_substep -> halo fill, 2 RK steps, every substep compared."""
+    n, dt = 16, 0.002
+    kw = dict(preset=preset, emulation=emulation, strategy=strategy)
+    s = b200_solver(b200, n, **kw)
+    c = checker(n, **kw)
+    s.init_tgv()
+    c.init()
+    for it in range(2):
+        for sub in range(3):
+            assert s.evaluate() is None
+            assert c.evaluate()[0] == 0
+            assert_state(s, c, (2,), f"{kw} it{it} sub{sub} R")
+            assert s.rk_substep(sub, dt) is None
+            c.rk_substep(sub, dt)
+            s.fill_state_halos()
+            assert_state(s, c, (0, 1), f"{kw} it{it} sub{sub} Q/Qt")
+
+
+@pytest.mark.parametrize("split", list(po.SPLITS))
+@pytest.mark.parametrize("viscous", [True, False])
+def test_splits(b200, split, viscous):
+    kw = dict(preset="HPSP", split=split, viscous=viscous, mach=0.4)
+    s = b200_solver(b200, 12, **kw)
+    c = checker(12, **kw)
+    s.init_tgv()
+    c.init()
+    r = s.advance(b200.StepConfig(0.004, 2, 0))
+    st, _, _, _ = c.advance(0.004, 2, 0)
+    assert not r.diverged and st == 0
+    assert_state(s, c, (0, 1), f"split {split} visc {viscous}")
+
+
+def test_overrides(b200):
+    """wk-array name overrides (precision.cpp:46-56) are honoured."""
+    ov = {"T": "B32", "dudx": "B32", "u": "B16"}
+    for strategy in STRATS:
+        kw = dict(preset="HPSP", strategy=strategy, overrides=ov)
+        s = b200_solver(b200, 12, **kw)
+        c = checker(12, **kw)
+        s.init_tgv()
+        c.init()
+        s.advance(b200.StepConfig(0.003, 2, 0))
+        c.advance(0.003, 2, 0)
+        assert_state(s, c, (0, 1), f"overrides {strategy}")
+
+
+@pytest.mark.parametrize("threads", [1, 8])
+@pytest.mark.parametrize("preset", ["DP", "SPDP", "HPSP"])
+def test_advance_series(b200, preset, threads):
+    """advance with sampling: identical K / enstrophy series (same tree)."""
+    n = 32
+    s = b200_solver(b200, n, preset)
+    c = checker(n, preset=preset, threads=threads) if po.ref_available() else checker(n, preset=preset)
+    s.init_tgv()
+    c.init()
+    r = s.advance(b200.StepConfig(0.002, 6, 2), threads=threads)
+    st, series, _, it = c.advance(0.002, 6, 2, threads=threads)
+    assert not r.diverged and st == 0 and r.iterations_run == it == 6
+    got = np.array([[x.t, x.kinetic_energy, x.enstrophy, x.eps_s] for x in r.series])
+    assert got.shape[0] == series.shape[0]
+    assert same_bits(got, series[:, :4])
+    assert_state(s, c, (0, 1), f"advance {preset}")
+
+
+def test_diagnostics_kat(b200):
+    """K(0) = 0.125, eps_S(0) at Re=800."""
+    s = b200_solver(b200, 64, "DP", mach=0.5, re=800.0)
+    s.init_tgv()
+    d = s.diagnostics(0, 0.0, 8)
+    assert abs(d.kinetic_energy - 0.125) < 1e-12
+    assert abs(d.eps_s - 9.375e-4) / 9.375e-4 < 1e-5
+
+
+@pytest.mark.parametrize("preset", ["DP", "HPSP", "HP"])
+def test_uniform_state_zero_residual(b200, preset):
+    """Uniform quiescent state -> R == 0 exactly."""
+    for strategy in STRATS:
+        s = b200_solver(b200, 16, preset, strategy=strategy)
+        s.init_uniform()
+        assert s.evaluate() is None
+        for comp in range(5):
+            assert np.all(s.get_field(2, comp) == 0.0)
+
+
+@pytest.mark.parametrize("preset", ["DP", "HP"])
+def test_divergence_event(b200, preset):
+    """Inviscid Divergence split blows up: same event, iteration and series."""
+    kw = dict(preset=preset, split="Divergence", viscous=False, mach=0.4)
+    s = b200_solver(b200, 16, **kw)
+    c = checker(16, **kw)
+    s.init_tgv()
+    c.init()
+    r = s.advance(b200.StepConfig(0.2, 400, 10))
+    st, series, ev, it = c.advance(0.2, 400, 10)
+    assert r.diverged and st == 2
+    e = r.divergence
+    assert [{"nonpositive or nonfinite density": 1, "nonfinite residual": 2,
+             "nonfinite state": 3}[e.what], e.i, e.j, e.k, e.iteration, e.substep] == ev
+    assert r.iterations_run == it
+    got = np.array([[x.t, x.kinetic_energy, x.enstrophy, x.eps_s, x.diverged] for x in r.series])
+    np.testing.assert_array_equal(np.isnan(got), np.isnan(series))
+    assert same_bits(np.nan_to_num(got), np.nan_to_num(series))
+    assert_state(s, c, (0, 1), "divergence")
+
+
+@pytest.mark.parametrize("pz", [2, 4])
+def test_local_slabs_bitwise(b200, pz):
+    """z-slab decomposition on one device: bitwise equal to one slab."""
+    n = 32
+    one = b200_solver(b200, n, "HPSP")
+    many = b200_solver(b200, n, "HPSP", decomp=b200.Decomposition(pz=pz))
+    one.init_tgv()
+    many.init_tgv()
+    r1 = one.advance(b200.StepConfig(0.002, 4, 2))
+    r2 = many.advance(b200.StepConfig(0.002, 4, 2))
+    for cls in (0, 1):
+        for comp in range(5):
+            assert same_bits(one.get_field(cls, comp), many.get_field(cls, comp))
+    a = [(x.kinetic_energy, x.enstrophy) for x in r1.series]
+    b = [(x.kinetic_energy, x.enstrophy) for x in r2.series]
+    assert a == b
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("preset", ["DP", "SPDP", "HPSP"])
+def test_64_cubed_step(b200, preset):
+    """One full RK step at 64^3 (config C1 size) against the reference."""
+    n = 64
+    s = b200_solver(b200, n, preset)
+    c = checker(n, preset=preset)
+    s.init_tgv()
+    c.init()
+    s.advance(b200.StepConfig(0.002, 1, 0))
+    c.advance(0.002, 1, 0)
+    assert_state(s, c, (0, 1), f"64^3 {preset}")
