@@ -181,6 +181,16 @@ int mpfd_b200_profile_read(mpfd_solver* s, double ms[4], long launches[4]);
  * reference's field set (memory_report, registry.cpp:24-39). */
 int mpfd_b200_memory(mpfd_solver* s, size_t* device_bytes, size_t* census_bytes,
                      size_t* census_b64_bytes);
+/* Halo plan of z-slab `rank` of `pz` for an n^3 grid with q storage of
+ * `bytes_q` bytes (pure host arithmetic, no device): the byte offsets into
+ * the slab's Q buffer ([nzl+8 planes][5][n][n]) of the block sent to the
+ * upper neighbour (top 4 interior planes), the block received into the lower
+ * ghost planes, the block sent down (bottom 4 interior planes) and the block
+ * received into the upper ghost planes; the block size; the upper and lower
+ * neighbour ranks; the slab's first global plane and its plane count.
+ * out[9] = {send_up, recv_lo, send_dn, recv_hi, block_bytes, up, dn, z0, nzl}. */
+int mpfd_b200_halo_plan(int n, int pz, int rank, int bytes_q, long long out[9]);
+
 /* Which residual path runs: 0 = staged multi-kernel, 1 = fused. */
 int mpfd_b200_set_path(mpfd_solver* s, int path);
 

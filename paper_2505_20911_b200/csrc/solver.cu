@@ -232,6 +232,33 @@ static std::unique_ptr<Launcher> make_launcher(const KernelPlan& p) {
 }
 
 // ---------------------------------------------------------------------------
+// z-halo plan of one slab (fill_halos_periodic's z pass, field.cpp:29-36,
+// distributed): send the top/bottom H interior planes of all 5 components,
+// receive into the lower/upper ghost planes.  Offsets in bytes into the
+// slab's Q buffer [nzl+2H][5][n][n].
+struct HaloPlan {
+    long long send_up, recv_lo, send_dn, recv_hi, block;
+    int up, dn, z0, nzl;
+};
+static HaloPlan halo_plan(int n, int pz, int rank, int bq) {
+    if (pz < 1 || n % pz != 0) throw ConfigError("grid n is not divisible by the z process count");
+    if (rank < 0 || rank >= pz) throw ConfigError("rank out of range");
+    HaloPlan p;
+    p.nzl = n / pz;
+    if (p.nzl < kHalo) throw ConfigError("z slab thinner than the halo depth (4)");
+    const long long plane5 = 5LL * n * n * bq;
+    p.block = kHalo * plane5;
+    p.send_up = (long long)p.nzl * plane5;           // planes [nzl, nzl+H)
+    p.recv_lo = 0;                                   // planes [0, H)
+    p.send_dn = p.block;                             // planes [H, 2H)
+    p.recv_hi = (long long)(p.nzl + kHalo) * plane5;  // planes [nzl+H, nzl+2H)
+    p.up = (rank + 1) % pz;
+    p.dn = (rank + pz - 1) % pz;
+    p.z0 = rank * p.nzl;
+    return p;
+}
+
+// ---------------------------------------------------------------------------
 // host reductions (reduce.cpp:14-36)
 static double pairwise_sum(const double* v, size_t n) {
     if (n <= 32) {
@@ -714,13 +741,14 @@ void Solver::halo_refresh() {
     if (mode == MPFD_DECOMP_NCCL && pz > 1) {
         Slab& s = slabs[0];
         CK(cudaSetDevice(s.device));
-        const size_t blk = (size_t)kHalo * 5 * s.geo.plane * bq;
+        const HaloPlan hp = halo_plan(n, pz, rank, (int)bq);
         char* q = (char*)qcur(s);
-        const int up = (rank + 1) % pz, dn = (rank + pz - 1) % pz;
-        char* top_int = q + (size_t)s.geo.nzl * 5 * s.geo.plane * bq;  // planes [nzl, nzl+H)
-        char* bot_int = q + blk;                                      // planes [H, 2H)
-        char* lo_ghost = q;                                           // planes [0, H)
-        char* hi_ghost = q + (size_t)(s.geo.nzl + kHalo) * 5 * s.geo.plane * bq;
+        const size_t blk = (size_t)hp.block;
+        const int up = hp.up, dn = hp.dn;
+        char* top_int = q + hp.send_up;
+        char* bot_int = q + hp.send_dn;
+        char* lo_ghost = q + hp.recv_lo;
+        char* hi_ghost = q + hp.recv_hi;
         Nccl& nc = Nccl::get();
         timed(2, s, [&] {
             nc.check(nc.groupStart(), "ncclGroupStart");
@@ -1394,6 +1422,15 @@ int mpfd_b200_memory(mpfd_solver* h, size_t* device_bytes, size_t* census, size_
             }
         if (census) *census = tot;
         if (census_b64) *census_b64 = cnt * pts * 8;
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_halo_plan(int n, int pz, int rank, int bytes_q, long long out[9]) {
+    return guard([&] {
+        const HaloPlan p = halo_plan(n, pz, rank, bytes_q);
+        const long long v[9] = {p.send_up, p.recv_lo, p.send_dn, p.recv_hi, p.block, p.up, p.dn, p.z0, p.nzl};
+        for (int i = 0; i < 9; ++i) out[i] = v[i];
         return MPFD_OK;
     });
 }
