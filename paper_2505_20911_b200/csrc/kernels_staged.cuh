@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(256) k_diag_integrand(Geo g, const QS* __restr
 // leaves of 32, then a perfect binary tree.  One warp per chunk: each lane
 // owns 4 consecutive leaves, the lane tree is a xor butterfly (IEEE addition
 // is commutative, so both partners hold the same bits).
-__global__ void k_chunk_sums(const double* __restrict__ v, long long nchunks, double* __restrict__ out) {
+static __global__ void k_chunk_sums(const double* __restrict__ v, long long nchunks, double* __restrict__ out) {
     const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= nchunks) return;

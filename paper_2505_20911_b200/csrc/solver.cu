@@ -29,8 +29,7 @@
 
 #include "../../include/mpfd_b200.h"
 #include "host_common.hpp"
-#include "kernels_fused.cuh"
-#include "kernels_staged.cuh"
+#include "launcher.cuh"
 
 namespace mpfd_b200 {
 
@@ -91,136 +90,6 @@ struct Nccl {
 };
 // ncclDataType_t values (nccl.h): ncclUint8 1, ncclInt32 2, ncclUint64 5, ncclFloat64 8
 // ncclRedOp_t: ncclSum 0, ncclMin 3
-
-template <int K>
-struct TypeOfK;
-template <>
-struct TypeOfK<0> {
-    using type = __half;
-};
-template <>
-struct TypeOfK<1> {
-    using type = float;
-};
-template <>
-struct TypeOfK<2> {
-    using type = double;
-};
-template <int K>
-using TypeOf = typename TypeOfK<K>::type;
-
-// ---------------------------------------------------------------------------
-// per-slab device state
-struct Slab {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    Geo geo{};
-    void* q = nullptr;     // [planes][5][ny][nx] QS
-    void* qt = nullptr;    // [nzl][5][ny][nx]   TS
-    void* r = nullptr;     // [nzl][5][ny][nx]   RS
-    void* q2 = nullptr;    // fused path: Q output buffer (double-buffered)
-    void* qt2 = nullptr;   // fused path: Qt output buffer
-    void* prim = nullptr;  // staged path
-    void* lev2 = nullptr;  // staged path
-    double* diag = nullptr;
-    double* partials = nullptr;
-    DevDiv* div = nullptr;
-    double* staging = nullptr;
-    size_t staging_elems = 0;
-    size_t bytes = 0;
-};
-
-struct KernelPlan {
-    int mode;
-    int qk, tk, rk, wk;  // storage kinds of Q, Qt, R and the wk class
-    int pk;              // staged primitives buffer kind
-};
-
-// launch tables, one instantiation per supported precision plan
-struct Launcher {
-    virtual ~Launcher() = default;
-    virtual void prim(const Slab& s, const PrimConsts& pc, int iter, int sub) = 0;
-    virtual void level2(const Slab& s, const ResConsts& rc, const StageConsts& sc, bool staged) = 0;
-    virtual void resid(const Slab& s, const ResConsts& rc, int iter, int sub) = 0;
-    virtual void rk(const Slab& s, const RkConsts& kc, int iter, int sub) = 0;
-    virtual void diag_integrand(const Slab& s, int which, int density, double r) = 0;
-    virtual bool fused_available() const = 0;
-    virtual void fused(const Slab& s, const void* qin, void* qout, const void* qtin, void* qtout,
-                       const PrimConsts& pc, const ResConsts& rc, const StageConsts& sc, bool staged,
-                       const RkConsts& kc, bool write_r, int iter, int sub) = 0;
-};
-
-static dim3 block2d() { return dim3(32, 8, 1); }
-static dim3 grid2d(const Geo& g, int planes) {
-    return dim3((unsigned)((g.nx + 31) / 32), (unsigned)((g.ny + 7) / 8), (unsigned)planes);
-}
-
-template <int MODE, int QK, int TK, int RK, int WK, int PK>
-struct LauncherT final : Launcher {
-    using QS = TypeOf<QK>;
-    using TS = TypeOf<TK>;
-    using RS = TypeOf<RK>;
-    using PT = TypeOf<PK>;
-    using WC = TypeOf<MODE == 0 ? WK : 2>;
-    using RCt = TypeOf<MODE == 0 ? RK : 2>;
-    using TC = TypeOf<MODE == 0 ? TK : 2>;
-    using QC = TypeOf<MODE == 0 ? QK : 2>;
-
-    void prim(const Slab& s, const PrimConsts& pc, int iter, int sub) override {
-        k_prim<QS, WC, PT><<<grid2d(s.geo, s.geo.planes), block2d(), 0, s.stream>>>(
-            s.geo, (const QS*)s.q, (PT*)s.prim, pc, s.div, iter, sub);
-    }
-    void level2(const Slab& s, const ResConsts& rc, const StageConsts& sc, bool staged) override {
-        if (staged)
-            k_level2<RCt, WC, PT, true><<<grid2d(s.geo, s.geo.nzl + 4), block2d(), 0, s.stream>>>(
-                s.geo, (const PT*)s.prim, (RCt*)s.lev2, rc, sc, s.div);
-        else
-            k_level2<RCt, WC, PT, false><<<grid2d(s.geo, s.geo.nzl + 4), block2d(), 0, s.stream>>>(
-                s.geo, (const PT*)s.prim, (RCt*)s.lev2, rc, sc, s.div);
-    }
-    void resid(const Slab& s, const ResConsts& rc, int iter, int sub) override {
-        k_resid<RCt, QS, PT, RS><<<grid2d(s.geo, s.geo.nzl), block2d(), 0, s.stream>>>(
-            s.geo, (const QS*)s.q, (const PT*)s.prim, (const RCt*)s.lev2, (RS*)s.r, rc, s.div, iter, sub);
-    }
-    void rk(const Slab& s, const RkConsts& kc, int iter, int sub) override {
-        const long long n = (long long)s.geo.nzl * s.geo.plane;
-        k_rk<QS, TS, RS, TC, QC><<<(unsigned)((n + 255) / 256), 256, 0, s.stream>>>(
-            s.geo, (QS*)s.q, (TS*)s.qt, (const RS*)s.r, kc, s.div, iter, sub);
-    }
-    void diag_integrand(const Slab& s, int which, int density, double r) override {
-        k_diag_integrand<QS><<<grid2d(s.geo, s.geo.nzl), block2d(), 0, s.stream>>>(
-            s.geo, (const QS*)s.q, s.diag, which, density, r);
-    }
-    bool fused_available() const override { return FusedPlan<MODE, QK, TK, RK, WK>::available; }
-    void fused(const Slab& s, const void* qin, void* qout, const void* qtin, void* qtout,
-               const PrimConsts& pc, const ResConsts& rc, const StageConsts& sc, bool staged,
-               const RkConsts& kc, bool write_r, int iter, int sub) override {
-        FusedPlan<MODE, QK, TK, RK, WK>::launch(s.geo, s.stream, qin, qout, qtin, qtout, s.r, pc, rc, sc,
-                                                staged, kc, write_r, s.div, iter, sub);
-    }
-};
-
-// supported precision plans: the reference's nine presets under both
-// emulation modes (precision.cpp:58-88).  mode, q, rk, res, wk, prim buffer.
-#define MPFD_PLANS(X)        \
-    X(0, 2, 2, 2, 2, 2)      \
-    X(0, 1, 1, 1, 1, 1)      \
-    X(0, 0, 0, 0, 0, 0)      \
-    X(0, 2, 2, 1, 1, 1)      \
-    X(0, 2, 2, 2, 1, 1)      \
-    X(0, 2, 2, 1, 2, 2)      \
-    X(0, 1, 1, 0, 0, 0)      \
-    X(0, 1, 1, 1, 0, 0)      \
-    X(0, 1, 1, 0, 1, 1)      \
-    X(1, 2, 2, 2, 2, 2)      \
-    X(1, 1, 1, 1, 1, 1)      \
-    X(1, 0, 0, 0, 0, 0)      \
-    X(1, 2, 2, 1, 1, 1)      \
-    X(1, 2, 2, 2, 1, 1)      \
-    X(1, 2, 2, 1, 2, 2)      \
-    X(1, 1, 1, 0, 0, 0)      \
-    X(1, 1, 1, 1, 0, 0)      \
-    X(1, 1, 1, 0, 1, 1)
 
 static std::unique_ptr<Launcher> make_launcher(const KernelPlan& p) {
 #define MPFD_TRY(m, q, t, r, w, pbuf)                                                         \
@@ -311,7 +180,8 @@ struct Solver {
     void reset_div();
 
     int nzl() const { return slabs.empty() ? 0 : slabs[0].geo.nzl; }
-    bool use_fused() const { return path == 1 && launch->fused_available(); }
+    bool fused_ok = false;  // fused kernels compiled for this plan and its wk overrides
+    bool use_fused() const { return path == 1 && fused_ok; }
     void* qcur(const Slab& s) const { return (use_fused() && qbuf) ? s.q2 : s.q; }
     void* qtcur(const Slab& s) const { return (use_fused() && qbuf) ? s.qt2 : s.qt; }
 
@@ -415,6 +285,9 @@ void Solver::setup(const mpfd_grid* grid, const mpfd_precision* p, int strategy_
     plan = {prec.emulation, prec.q, prec.rk, prec.res, prec.wk,
             prec.emulation == 0 ? prec.wk : pk};
     launch = make_launcher(plan);
+    // the fused kernel carries primitives in the wk class type: a StoreRound
+    // override wider than the class would not fit (the staged path handles it)
+    fused_ok = launch && launch->fused_available() && (plan.mode == 0 || plan.pk == plan.wk);
     if (!launch)
         throw ConfigError("B200 backend: precision combination not compiled (supported: the nine "
                           "presets DP SP HP SPDP SPDP-wk SPDP-res HPSP HPSP-wk HPSP-res, strict or "
@@ -471,7 +344,7 @@ void Solver::alloc() {
         get(&s.q, qel * bq);
         get(&s.qt, iel * bt);
         get(&s.r, iel * br);
-        if (launch->fused_available()) {
+        if (fused_ok) {
             get(&s.q2, qel * bq);
             get(&s.qt2, iel * bt);
         }
@@ -485,7 +358,7 @@ void Solver::alloc() {
         CK(cudaMalloc(&s.staging, s.staging_elems * sizeof(double)));
         s.bytes += s.staging_elems * sizeof(double);
     }
-    if (!launch->fused_available()) path = 0;
+    if (!fused_ok) path = 0;
     CK(cudaHostAlloc(&pinned_flag, sizeof(int) * 64, cudaHostAllocDefault));
     reset_div();
     sync();
@@ -1438,7 +1311,7 @@ int mpfd_b200_halo_plan(int n, int pz, int rank, int bytes_q, long long out[9]) 
 int mpfd_b200_set_path(mpfd_solver* h, int path) {
     return guard([&] {
         Solver& S = h->s;
-        if (path == 1 && !S.launch->fused_available()) throw ConfigError("fused path not available for this precision plan");
+        if (path == 1 && !S.fused_ok) throw ConfigError("fused path not available for this precision plan");
         if (path != S.path) {
             // move the state into the primary buffers before switching
             if (S.path == 1 && S.qbuf) {

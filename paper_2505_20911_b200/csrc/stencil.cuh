@@ -81,16 +81,18 @@ __device__ __forceinline__ T phi_val(const Acc& a, int phi, int d, int s) {
     return a.U(phi - 1, d, s);
 }
 
-// C_j(phi) at the center, conv_term_point (physics.cpp:93-155)
-template <class T, class Acc>
+// C_j(phi) at the center, conv_term_point (physics.cpp:93-155).  SPL != 0
+// fixes the active-term mask at compile time (same terms, same order).
+template <class T, unsigned SPL = 0, class Acc>
 __device__ __forceinline__ T conv_term(const RC<T>& c, const Acc& a, int phi, int j) {
     using O = Op<T>;
+    const unsigned nzm = SPL ? SPL : c.nz;
     const T uj0 = a.U(j, j, 0);
     const T rho0 = a.Q(0, j, 0);
-    const bool need_phi0 = (c.nz & 0x18u) && phi != 0;
+    const bool need_phi0 = (nzm & 0x18u) && phi != 0;
     const T phi0 = need_phi0 ? phi_val<T>(a, phi, j, 0) : O::one();
     T acc = O::zero();
-    if (c.nz & 0x01u) {  // alpha d(rho u_j phi)
+    if (nzm & 0x01u) {  // alpha d(rho u_j phi)
         const T t = d1<T>(
             [&](int s) {
                 if (phi == 0) return a.Q(1 + j, j, s);
@@ -100,7 +102,7 @@ __device__ __forceinline__ T conv_term(const RC<T>& c, const Acc& a, int phi, in
             c.r);
         acc = O::add(acc, O::mul(c.coef[0], t));
     }
-    if (c.nz & 0x02u) {  // beta_rho rho d(u_j phi)
+    if (nzm & 0x02u) {  // beta_rho rho d(u_j phi)
         const T t = d1<T>(
             [&](int s) {
                 if (phi == 0) return a.U(j, j, s);
@@ -109,88 +111,221 @@ __device__ __forceinline__ T conv_term(const RC<T>& c, const Acc& a, int phi, in
             c.r);
         acc = O::add(acc, O::mul(c.coef[1], O::mul(rho0, t)));
     }
-    if (c.nz & 0x04u) {  // beta_u u_j d(rho phi)
+    if (nzm & 0x04u) {  // beta_u u_j d(rho phi)
         const T t = d1<T>([&](int s) { return a.Q(phi, j, s); }, c.r);
         acc = O::add(acc, O::mul(c.coef[2], O::mul(uj0, t)));
     }
-    if (c.nz & 0x08u) {  // beta_phi phi d(rho u_j)
+    if (nzm & 0x08u) {  // beta_phi phi d(rho u_j)
         const T t = d1<T>([&](int s) { return a.Q(1 + j, j, s); }, c.r);
         acc = O::add(acc, O::mul(c.coef[3], phi == 0 ? t : O::mul(phi0, t)));
     }
-    if (c.nz & 0x10u) {  // gamma_rho u_j phi d(rho)
+    if (nzm & 0x10u) {  // gamma_rho u_j phi d(rho)
         const T t = d1<T>([&](int s) { return a.Q(0, j, s); }, c.r);
         const T uphi = phi == 0 ? uj0 : O::mul(uj0, phi0);
         acc = O::add(acc, O::mul(c.coef[4], O::mul(uphi, t)));
     }
-    if (c.nz & 0x20u) {  // gamma_u rho phi d(u_j)
+    if (nzm & 0x20u) {  // gamma_u rho phi d(u_j)
         const T t = d1<T>([&](int s) { return a.U(j, j, s); }, c.r);
         acc = O::add(acc, O::mul(c.coef[5], O::mul(a.Q(phi, j, 0), t)));
     }
-    if ((c.nz & 0x40u) && phi != 0) {  // gamma_phi rho u_j d(phi)
+    if ((nzm & 0x40u) && phi != 0) {  // gamma_phi rho u_j d(phi)
         const T t = d1<T>([&](int s) { return phi_val<T>(a, phi, j, s); }, c.r);
         acc = O::add(acc, O::mul(c.coef[6], O::mul(a.Q(1 + j, j, 0), t)));
     }
     return acc;
 }
 
-// viscous_momentum (physics.cpp:224-233) with div u read as a level-2 field
+// The fused residual at one point (residual_slab, physics.cpp:345-394),
+// split in two so a z-marching kernel can evaluate it at two lags:
+//   early: every term except the z-derivatives of the level-2 fields --
+//          R_rho, R_rhou, R_rhov complete; for R_rhow and R_rhoE the partial
+//          values the reference has formed before adding those terms;
+//   late:  d/dz of div u (momentum w), of sum_i u_i tau_iz and of dT/dz
+//          (energy), added in the reference's order.
+// residual_point composes both, so every kernel shares one operation order.
+template <class T>
+struct Deferred {
+    T val0_w;  // -C(w) - dp/dz
+    T lap_w;   // d2w/dx2 + d2w/dy2 + d2w/dz2
+    T val0_E;  // -C(E) - d(p u_j)/dx_j
+    T tau_xy;  // 0 + d(g_x)/dx + d(g_y)/dy
+    T h_xy;    // 0 + d(dT/dx)/dx + d(dT/dy)/dy
+};
+
 template <class T, class Acc>
-__device__ __forceinline__ T visc_momentum(const RC<T>& c, const Acc& a, int i) {
+__device__ __forceinline__ T momentum_lap(const RC<T>& c, const Acc& a, int i) {
     using O = Op<T>;
     T l[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d)
         l[d] = d2v<T>(a.U(i, d, -2), a.U(i, d, -1), a.U(i, d, 0), a.U(i, d, 1), a.U(i, d, 2), c.r2);
-    const T lap = O::add(O::add(l[0], l[1]), l[2]);
-    const T cross = d1<T>([&](int s) { return a.DIVU(i, s); }, c.r);
-    return O::mul(c.inv_re, O::add(lap, O::mul(c.third, cross)));
+    return O::add(O::add(l[0], l[1]), l[2]);
 }
 
-// the fused residual at one point (residual_slab, physics.cpp:345-394)
-template <class T, class Acc>
-__device__ __forceinline__ void residual_point(const RC<T>& c, const Acc& a, T out[5]) {
+template <class T, unsigned SPL = 0, class Acc>
+__device__ __forceinline__ void residual_early(const RC<T>& c, const Acc& a, T out[3], Deferred<T>& df) {
     using O = Op<T>;
     {
-        const T cx = conv_term<T>(c, a, 0, 0);
-        const T cy = conv_term<T>(c, a, 0, 1);
-        const T cz = conv_term<T>(c, a, 0, 2);
+        const T cx = conv_term<T, SPL>(c, a, 0, 0);
+        const T cy = conv_term<T, SPL>(c, a, 0, 1);
+        const T cz = conv_term<T, SPL>(c, a, 0, 2);
         out[0] = O::neg(O::add(O::add(cx, cy), cz));
     }
-#pragma unroll 1
+#pragma unroll
     for (int m = 0; m < 3; ++m) {
-        const T cx = conv_term<T>(c, a, 1 + m, 0);
-        const T cy = conv_term<T>(c, a, 1 + m, 1);
-        const T cz = conv_term<T>(c, a, 1 + m, 2);
+        const T cx = conv_term<T, SPL>(c, a, 1 + m, 0);
+        const T cy = conv_term<T, SPL>(c, a, 1 + m, 1);
+        const T cz = conv_term<T, SPL>(c, a, 1 + m, 2);
         const T conv = O::add(O::add(cx, cy), cz);
         const T dp = d1<T>([&](int s) { return a.P(m, s); }, c.r);
-        T val = O::sub(O::neg(conv), dp);
-        if (c.viscous) val = O::add(val, visc_momentum<T>(c, a, m));
-        out[1 + m] = val;
+        const T val0 = O::sub(O::neg(conv), dp);
+        if (m < 2) {
+            T val = val0;
+            if (c.viscous) {
+                // viscous_momentum (physics.cpp:224-233)
+                const T lap = momentum_lap<T>(c, a, m);
+                const T cross = d1<T>([&](int s) { return a.DIVU(m, s); }, c.r);
+                val = O::add(val, O::mul(c.inv_re, O::add(lap, O::mul(c.third, cross))));
+            }
+            out[1 + m] = val;
+        } else {
+            df.val0_w = val0;
+            df.lap_w = c.viscous ? momentum_lap<T>(c, a, 2) : O::zero();
+        }
     }
     {
-        const T cx = conv_term<T>(c, a, 4, 0);
-        const T cy = conv_term<T>(c, a, 4, 1);
-        const T cz = conv_term<T>(c, a, 4, 2);
+        const T cx = conv_term<T, SPL>(c, a, 4, 0);
+        const T cy = conv_term<T, SPL>(c, a, 4, 1);
+        const T cz = conv_term<T, SPL>(c, a, 4, 2);
         const T conv = O::add(O::add(cx, cy), cz);
         T pw = O::zero();
 #pragma unroll
         for (int d = 0; d < 3; ++d)
             pw = O::add(pw, d1<T>([&](int s) { return O::mul(a.P(d, s), a.U(d, d, s)); }, c.r));
-        T val = O::sub(O::neg(conv), pw);
+        df.val0_E = O::sub(O::neg(conv), pw);
+        df.tau_xy = O::zero();
+        df.h_xy = O::zero();
         if (c.viscous) {
+            // viscous_energy_tau / viscous_energy_heat (physics.cpp:236-271), x and y terms
             T tau = O::zero();
-#pragma unroll
-            for (int j = 0; j < 3; ++j)
-                tau = O::add(tau, d1<T>([&](int s) { return a.G(j, j, s); }, c.r));
+            tau = O::add(tau, d1<T>([&](int s) { return a.G(0, 0, s); }, c.r));
+            tau = O::add(tau, d1<T>([&](int s) { return a.G(1, 1, s); }, c.r));
             T h = O::zero();
-#pragma unroll
-            for (int j = 0; j < 3; ++j)
-                h = O::add(h, d1<T>([&](int s) { return a.DT(j, j, s); }, c.r));
-            val = O::add(val, tau);
-            val = O::add(val, O::mul(c.kappa, h));
+            h = O::add(h, d1<T>([&](int s) { return a.DT(0, 0, s); }, c.r));
+            h = O::add(h, d1<T>([&](int s) { return a.DT(1, 1, s); }, c.r));
+            df.tau_xy = tau;
+            df.h_xy = h;
         }
-        out[4] = val;
     }
+}
+
+// One axis' worth of neighbour values in registers (offsets -2..2), so every
+// term along that axis reads registers instead of re-loading shared memory.
+// Only queries along axis J are valid -- exactly what conv_term issues.
+template <class T>
+struct DirVals {
+    T q[5][5], u[3][5], p[5];
+    __device__ __forceinline__ T Q(int c, int, int s) const { return q[c][s + 2]; }
+    __device__ __forceinline__ T U(int m, int, int s) const { return u[m][s + 2]; }
+    __device__ __forceinline__ T P(int, int s) const { return p[s + 2]; }
+};
+
+template <class T, class Acc>
+__device__ __forceinline__ void load_dir(const Acc& a, int j, DirVals<T>& v) {
+#pragma unroll
+    for (int s = -2; s <= 2; ++s) {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) v.q[c][s + 2] = a.Q(c, j, s);
+#pragma unroll
+        for (int m = 0; m < 3; ++m) v.u[m][s + 2] = a.U(m, j, s);
+        v.p[s + 2] = a.P(j, s);
+    }
+}
+
+// residual_early evaluated axis by axis (same values, same operations; only
+// the order in which independent terms are formed differs).  Terms along
+// axis j: C_j(phi) for all phi, dp/dx_j, d(p u_j)/dx_j, d2 u_i/dx_j^2, and
+// for the in-plane axes the level-2 stencils d(div u)/dx_j,
+// d(sum u tau_.j)/dx_j and d(dT/dx_j)/dx_j.
+template <class T, unsigned SPL = 0, class Acc>
+__device__ __forceinline__ void residual_early_dirwise(const RC<T>& c, const Acc& a, T out[3], Deferred<T>& df) {
+    using O = Op<T>;
+    T C[5][3], dp[3], pwj[3], lap[3][3], cross[2], tauj[2], hj[2];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        DirVals<T> v;
+        load_dir<T>(a, j, v);
+#pragma unroll
+        for (int phi = 0; phi < 5; ++phi) C[phi][j] = conv_term<T, SPL>(c, v, phi, j);
+        dp[j] = d1v<T>(v.p[0], v.p[1], v.p[3], v.p[4], c.r);
+        pwj[j] = d1v<T>(O::mul(v.p[0], v.u[j][0]), O::mul(v.p[1], v.u[j][1]), O::mul(v.p[3], v.u[j][3]),
+                        O::mul(v.p[4], v.u[j][4]), c.r);
+        if (c.viscous) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                lap[i][j] = d2v<T>(v.u[i][0], v.u[i][1], v.u[i][2], v.u[i][3], v.u[i][4], c.r2);
+            if (j < 2) {
+                cross[j] = d1<T>([&](int s) { return a.DIVU(j, s); }, c.r);
+                tauj[j] = d1<T>([&](int s) { return a.G(j, j, s); }, c.r);
+                hj[j] = d1<T>([&](int s) { return a.DT(j, j, s); }, c.r);
+            }
+        }
+    }
+    out[0] = O::neg(O::add(O::add(C[0][0], C[0][1]), C[0][2]));
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+        const T conv = O::add(O::add(C[1 + m][0], C[1 + m][1]), C[1 + m][2]);
+        const T val0 = O::sub(O::neg(conv), dp[m]);
+        const T lp = c.viscous ? O::add(O::add(lap[m][0], lap[m][1]), lap[m][2]) : O::zero();
+        if (m < 2) {
+            T val = val0;
+            if (c.viscous) val = O::add(val, O::mul(c.inv_re, O::add(lp, O::mul(c.third, cross[m]))));
+            out[1 + m] = val;
+        } else {
+            df.val0_w = val0;
+            df.lap_w = lp;
+        }
+    }
+    {
+        const T conv = O::add(O::add(C[4][0], C[4][1]), C[4][2]);
+        const T pw = O::add(O::add(O::add(O::zero(), pwj[0]), pwj[1]), pwj[2]);
+        df.val0_E = O::sub(O::neg(conv), pw);
+        df.tau_xy = O::zero();
+        df.h_xy = O::zero();
+        if (c.viscous) {
+            df.tau_xy = O::add(O::add(O::zero(), tauj[0]), tauj[1]);
+            df.h_xy = O::add(O::add(O::zero(), hj[0]), hj[1]);
+        }
+    }
+}
+
+// cross_w = d(div u)/dz, tz = d(sum_i u_i tau_iz)/dz, hz = d(dT/dz)/dz
+template <class T>
+__device__ __forceinline__ void residual_late(const RC<T>& c, const Deferred<T>& df, T cross_w, T tz, T hz,
+                                              T& r_w, T& r_E) {
+    using O = Op<T>;
+    if (!c.viscous) {
+        r_w = df.val0_w;
+        r_E = df.val0_E;
+        return;
+    }
+    r_w = O::add(df.val0_w, O::mul(c.inv_re, O::add(df.lap_w, O::mul(c.third, cross_w))));
+    const T tau = O::add(df.tau_xy, tz);
+    const T h = O::add(df.h_xy, hz);
+    r_E = O::add(O::add(df.val0_E, tau), O::mul(c.kappa, h));
+}
+
+template <class T, class Acc>
+__device__ __forceinline__ void residual_point(const RC<T>& c, const Acc& a, T out[5]) {
+    Deferred<T> df;
+    residual_early<T>(c, a, out, df);
+    T cw = Op<T>::zero(), tz = Op<T>::zero(), hz = Op<T>::zero();
+    if (c.viscous) {
+        cw = d1<T>([&](int s) { return a.DIVU(2, s); }, c.r);
+        tz = d1<T>([&](int s) { return a.G(2, 2, s); }, c.r);
+        hz = d1<T>([&](int s) { return a.DT(2, 2, s); }, c.r);
+    }
+    residual_late<T>(c, df, cw, tz, hz, out[3], out[4]);
 }
 
 // level-2 fields at one point from the 9 velocity gradients G[i*3+j] and the

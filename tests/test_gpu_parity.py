@@ -217,3 +217,35 @@ def test_64_cubed_step(b200, preset):
     s.advance(b200.StepConfig(0.002, 1, 0))
     c.advance(0.002, 1, 0)
     assert_state(s, c, (0, 1), f"64^3 {preset}")
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("emulation", EMUL)
+@pytest.mark.parametrize("preset", PRESETS)
+def test_fused_path_bitwise(b200, preset, emulation, strategy):
+    """The fused residual + RK kernel over 2 steps (6 substeps) on a grid
+    that is not a multiple of the 32x8 tile, plus R of the last substep."""
+    n, dt = 20, 0.002
+    kw = dict(preset=preset, emulation=emulation, strategy=strategy)
+    s = b200_solver(b200, n, path="fused", **kw)
+    c = checker(n, **kw)
+    s.init_tgv()
+    c.init()
+    r = s.advance(b200.StepConfig(dt, 2, 0))
+    st, _, _, _ = c.advance(dt, 2, 0)
+    assert not r.diverged and st == 0
+    assert_state(s, c, (0, 1, 2), f"fused {kw}")
+
+
+@pytest.mark.parametrize("pz", [1, 2])
+@pytest.mark.parametrize("path", ["fused", "staged"])
+def test_paths_agree_64(b200, path, pz):
+    """Both paths, one and two slabs, 3 steps at 64^3 DP and HPSP."""
+    for preset in ("DP", "HPSP"):
+        s = b200_solver(b200, 64, preset, path=path, decomp=b200.Decomposition(pz=pz))
+        c = checker(64, preset=preset)
+        s.init_tgv()
+        c.init()
+        s.advance(b200.StepConfig(0.002, 3, 0))
+        c.advance(0.002, 3, 0)
+        assert_state(s, c, (0, 1), f"{path} pz{pz} {preset}")
