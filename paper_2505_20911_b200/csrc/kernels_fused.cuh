@@ -22,6 +22,8 @@
 // bitwise those of the staged path and of the reference.
 #pragma once
 
+#include <type_traits>
+
 #include "kernels_staged.cuh"
 
 namespace mpfd_b200 {
@@ -161,15 +163,18 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
     // register windows along z (own column): level-2 z-operands of planes
     // t-6..t-2 and the deferred early partials of planes t-4..t-2
     T wdiv[5], wgz[5], wdt[5];
-    Deferred<T> dfr[3];
+    Deferred<T> dfr[2];
 #pragma unroll
     for (int i = 0; i < 5; ++i) wdiv[i] = wgz[i] = wdt[i] = Op<T>::zero();
 
     // rim points of this thread (phase A) and their wrapped in-plane offsets;
     // Q of the next plane is prefetched into registers one iteration ahead
     constexpr int KPF = (TL::R4N + TL::NT - 1) / TL::NT;
-    long long rim_off[KPF];
-    QS pf[KPF][5];
+    // when primitives and residual compute in the same type, Q is narrowed
+    // once on arrival (the only two uses both narrow to that type)
+    using PFT = typename std::conditional<std::is_same<WC, T>::value, T, QS>::type;
+    int rim_off[KPF];
+    PFT pf[KPF][5];
     const bool fastwrap = g.nx >= TL::TX + 8 && g.ny >= TL::TY + 8;
 #pragma unroll
     for (int k = 0; k < KPF; ++k) {
@@ -187,10 +192,10 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             yy %= g.ny;
             if (yy < 0) yy += g.ny;
         }
-        rim_off[k] = (long long)yy * g.nx + xx;
+        rim_off[k] = yy * g.nx + xx;
         const QS* qp = qin + (long long)(zs - 4 + kHalo) * 5 * g.plane + rim_off[k];
 #pragma unroll
-        for (int cc = 0; cc < 5; ++cc) pf[k][cc] = qp[cc * g.plane];
+        for (int cc = 0; cc < 5; ++cc) pf[k][cc] = cvt<PFT>(qp[cc * g.plane]);
     }
 
     int slot = 0;  // ring slot of plane t
@@ -206,12 +211,12 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             const int i = tid + k * TL::NT;
             if (i >= TL::R4N) break;
             const int ry = i / TL::R4X, rx = i - ry * TL::R4X;
-            const QS q0 = pf[k][0], q1 = pf[k][1], q2 = pf[k][2], q3 = pf[k][3], q4 = pf[k][4];
+            const PFT q0 = pf[k][0], q1 = pf[k][1], q2 = pf[k][2], q3 = pf[k][3], q4 = pf[k][4];
             // prefetch plane t+1 for this point (consumed next iteration)
             if (t + 1 < ze + 4) {
                 const QS* qp = qin + (long long)(t + 1 + kHalo) * 5 * g.plane + rim_off[k];
 #pragma unroll
-                for (int cc = 0; cc < 5; ++cc) pf[k][cc] = qp[cc * g.plane];
+                for (int cc = 0; cc < 5; ++cc) pf[k][cc] = cvt<PFT>(qp[cc * g.plane]);
             }
             using O = Op<WC>;
             const WC rho = cvt<WC>(q0);
@@ -333,31 +338,8 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
         }
         __syncthreads();
 
-        // ---- C: early residual of plane t-2 -> RK of rho, rhou, rhov --------
-        if (t >= zs + 2) {
-#pragma unroll
-            for (int i = 0; i < 2; ++i) dfr[i] = dfr[i + 1];
-        }
-        if (t >= zs + 2 && t < ze + 2) {
-            if (own) {
-                RingAcc<T, PT, TL> acc;
-#pragma unroll
-                for (int i = 0; i < 5; ++i) {
-                    acc.pp[i] = plp[i] + p4;
-                    acc.prs[i] = Ppr + sl[i] * TL::R2N + p2;
-                    acc.qp[i] = Qr + sl[i] * TL::R2N + p2;
-                }
-                acc.lp = Lb + p2;
-                T out[3];
-                residual_early_dirwise<T, SPL>(c, acc, out, dfr[2]);
-                const int cpl = t - 2;
-#pragma unroll
-                for (int comp = 0; comp < 3; ++comp)
-                    rk_point<QS, TS, RS, TC, QC>(a, comp, cpl, o, cvt<RS>(out[comp]), x, y);
-            }
-        }
-
         // ---- D: late residual of plane t-4 -> RK of rhow, rhoE ---------------
+        // (runs before C so its deferred slot can be reused for plane t-2)
         if (t >= zs + 4 && own) {
             T cw = Op<T>::zero(), tz = Op<T>::zero(), hz = Op<T>::zero();
             if (c.viscous) {
@@ -370,6 +352,26 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             const int cpl = t - 4;
             rk_point<QS, TS, RS, TC, QC>(a, 3, cpl, o, cvt<RS>(rw_), x, y);
             rk_point<QS, TS, RS, TC, QC>(a, 4, cpl, o, cvt<RS>(rE), x, y);
+        }
+        // deferred window: dfr[0] plane t-3, dfr[1] plane t-2 after this step
+        if (t >= zs + 2) dfr[0] = dfr[1];
+
+        // ---- C: early residual of plane t-2 -> RK of rho, rhou, rhov --------
+        if (t >= zs + 2 && t < ze + 2 && own) {
+            RingAcc<T, PT, TL> acc;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                acc.pp[i] = plp[i] + p4;
+                acc.prs[i] = Ppr + sl[i] * TL::R2N + p2;
+                acc.qp[i] = Qr + sl[i] * TL::R2N + p2;
+            }
+            acc.lp = Lb + p2;
+            T out[3];
+            residual_early_dirwise<T, SPL>(c, acc, out, dfr[1]);
+            const int cpl = t - 2;
+#pragma unroll
+            for (int comp = 0; comp < 3; ++comp)
+                rk_point<QS, TS, RS, TC, QC>(a, comp, cpl, o, cvt<RS>(out[comp]), x, y);
         }
         __syncthreads();
         // rotate the ring: planes t-3..t+1
@@ -386,91 +388,6 @@ template <class T, class PT>
 struct FusedTile {
     using TL = Tile<32, 8>;
     static constexpr int MINB = sizeof(T) >= 8 || sizeof(PT) >= 8 ? 1 : 2;
-};
-
-template <int K>
-struct KT;
-template <>
-struct KT<0> {
-    using type = __half;
-};
-template <>
-struct KT<1> {
-    using type = float;
-};
-template <>
-struct KT<2> {
-    using type = double;
-};
-
-template <int MODE, int QK, int TK, int RK, int WK>
-struct FusedPlan {
-    static constexpr bool available = true;
-    using QS = typename KT<QK>::type;
-    using TS = typename KT<TK>::type;
-    using RS = typename KT<RK>::type;
-    using WC = typename KT<MODE == 0 ? WK : 2>::type;
-    using T = typename KT<MODE == 0 ? RK : 2>::type;
-    using TC = typename KT<MODE == 0 ? TK : 2>::type;
-    using QC = typename KT<MODE == 0 ? QK : 2>::type;
-    // exact carrier of every stored primitive: wk compute (Strict) or the wk
-    // storage (StoreRound; per-name overrides wider than the class are
-    // rejected for the fused path by the host)
-    using PT = typename KT<WK>::type;
-    using FT = FusedTile<T, PT>;
-    using TL = typename FT::TL;
-
-    template <bool ST, unsigned SPL>
-    static void go(const FusedArgs& a, cudaStream_t st) {
-        auto kern = k_fused<QS, TS, RS, PT, WC, T, TC, QC, ST, TL, FT::MINB, SPL>;
-        constexpr size_t smem = FusedSmem<TL, T, PT>::total;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
-        const dim3 grid((a.g.nx + TL::TX - 1) / TL::TX, (a.g.ny + TL::TY - 1) / TL::TY,
-                        (a.g.nzl + a.lz - 1) / a.lz);
-        kern<<<grid, TL::NT, smem, st>>>(a);
-    }
-
-    static void launch(const Geo& g, cudaStream_t st, const void* qin, void* qout, const void* qtin, void* qtout,
-                       void* r, const PrimConsts& pc, const ResConsts& rc, const StageConsts& sc, bool staged,
-                       const RkConsts& kc, bool write_r, DevDiv* div, int iter, int sub) {
-        FusedArgs a;
-        a.g = g;
-        a.qin = qin;
-        a.qout = qout;
-        a.qtin = qtin;
-        a.qtout = qtout;
-        a.r = r;
-        a.pc = pc;
-        a.rc = rc;
-        a.sc = sc;
-        a.kc = kc;
-        a.write_r = write_r ? 1 : 0;
-        a.div = div;
-        a.iter = iter;
-        a.sub = sub;
-        // z-range per CTA: enough CTAs for ~8 waves of the 148 SMs, but at
-        // least 16 planes so the 8-plane start-up stays small
-        const long long cols = (long long)((g.nx + TL::TX - 1) / TL::TX) * ((g.ny + TL::TY - 1) / TL::TY);
-        int nzs = (int)std::max<long long>(1, (148LL * FT::MINB * 8 + cols - 1) / cols);
-        int lz = (g.nzl + nzs - 1) / nzs;
-        lz = std::max(lz, std::min(16, g.nzl));
-        a.lz = lz;
-        // the reference's default split (Blaisdell: alpha, beta_u, gamma_u) is
-        // compiled with its term mask fixed; any other split runs the generic
-        // runtime-masked kernel (same arithmetic, physics.cpp:93-155)
-        constexpr unsigned kBlaisdell = 0x25u;
-        if (rc.nz == kBlaisdell) {
-            if (staged) go<true, kBlaisdell>(a, st);
-            else go<false, kBlaisdell>(a, st);
-        } else {
-            if (staged) go<true, 0u>(a, st);
-            else go<false, 0u>(a, st);
-        }
-    }
 };
 
 }  // namespace mpfd_b200
