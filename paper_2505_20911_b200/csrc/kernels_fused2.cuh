@@ -403,7 +403,8 @@ struct FusedPlan {
 
     template <bool ST, unsigned SPL>
     static void go(FusedArgs a, cudaStream_t st) {
-        if (PAIR && a.g.nx % 2 == 0) {
+        if constexpr (PAIR) {
+            if (a.g.nx % 2 == 0) {
             auto kern = k_fused2<QS, TS, RS, PT, WC, T, TC, QC, ST, TL2, MINB2, SPL>;
             constexpr size_t smem = FusedSmem<TL2, T, PT>::total;
             static bool attr = false;
@@ -416,6 +417,7 @@ struct FusedPlan {
                             (a.g.nzl + a.lz - 1) / a.lz);
             kern<<<grid, TL2::NT / 2, smem, st>>>(a);
             return;
+            }
         }
         auto kern = k_fused<QS, TS, RS, PT, WC, T, TC, QC, ST, TL, FT::MINB, SPL>;
         constexpr size_t smem = FusedSmem<TL, T, PT>::total;

@@ -1,0 +1,69 @@
+"""CLI level: `mpfd run <cfg>` (reference, oracle/_ref/mpfd) and the B200
+drop-in `tools/mpfd_b200_run run <cfg>` write byte-identical diagnostics
+CSVs (io.cpp:19-36) and the same exit codes (tools/mpfd.cpp:4-5)."""
+import os
+import subprocess
+
+import pytest
+
+import pyoracle as po
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOOL = os.path.join(ROOT, "tools", "mpfd_b200_run")
+REF_CLI = os.path.join(ROOT, "oracle", "_ref", "mpfd")
+
+
+def build_tool(b200):
+    src = os.path.join(ROOT, "tools", "mpfd_b200_run.cpp")
+    if not os.path.exists(TOOL) or os.path.getmtime(TOOL) < max(
+            os.path.getmtime(src), os.path.getmtime(b200.library_path)):
+        subprocess.run(["g++", "-O2", "-std=c++17", "-I" + os.path.join(ROOT, "include"), src,
+                        "-L" + os.path.dirname(b200.library_path), "-lmpfd_b200",
+                        "-Wl,-rpath," + os.path.dirname(b200.library_path), "-o", TOOL], check=True)
+    return TOOL
+
+
+def test_tool_builds_and_rejects_bad_config(b200, tmp_path):
+    tool = build_tool(b200)
+    bad = tmp_path / "bad.cfg"
+    bad.write_text("nonsense_key = 42\n")  # tests/data/bad.cfg of the reference
+    r = subprocess.run([tool, "run", str(bad)], capture_output=True, text=True)
+    assert r.returncode == 1 and "unknown key" in r.stderr
+
+
+@pytest.mark.skipif(not os.path.exists(REF_CLI), reason="reference CLI not built")
+def test_reference_cli_exit_codes(tmp_path):
+    bad = tmp_path / "bad.cfg"
+    bad.write_text("nonsense_key = 42\n")
+    assert subprocess.run([REF_CLI, "run", str(bad)], capture_output=True).returncode == 1
+
+
+CFGS = {
+    "smoke_uniform": "case = uniform\nn = 8\ndt = 0.01\nn_iterations = 3\ndiagnostics_interval = 1\n",
+    "tgv_dp": "n = 32\nM = 0.1\nRe = 1600\ndt = 0.002\nn_iterations = 40\ndiagnostics_interval = 10\n"
+              "strategy = storesome\n",
+    "tgv_hpsp_default": "n = 32\nprecision = HPSP\ndt = 0.002\nn_iterations = 30\n"
+                        "diagnostics_interval = 10\nthreads = 4\n",
+    "tgv_spdp_storeround": "n = 24\nprecision = SPDP\nemulation = storeround\ndt = 0.003\n"
+                           "n_iterations = 20\ndiagnostics_interval = 5\nsplit = KGP\n",
+    "diverge": "n = 16\nM = 0.4\nviscous = false\nsplit = Divergence\ndt = 0.2\nn_iterations = 400\n"
+               "diagnostics_interval = 10\nstrategy = storesome\n",
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(REF_CLI), reason="reference CLI not built")
+@pytest.mark.parametrize("name", list(CFGS))
+def test_csv_byte_identical(b200, tmp_path, name):
+    tool = build_tool(b200)
+    outs = {}
+    codes = {}
+    for who, exe in (("ref", REF_CLI), ("b200", tool)):
+        cfg = tmp_path / f"{who}.cfg"
+        out = tmp_path / f"{who}.csv"
+        cfg.write_text(CFGS[name] + f"output = {out}\n")
+        r = subprocess.run([exe, "run", str(cfg)], capture_output=True, text=True, cwd=tmp_path)
+        codes[who] = r.returncode
+        outs[who] = out.read_bytes()
+    assert codes["ref"] == codes["b200"]
+    assert outs["ref"] == outs["b200"]
