@@ -28,6 +28,16 @@
 
 namespace mpfd_b200 {
 
+// primitive store rounding, skipped when provably the identity
+template <class W>
+__device__ __forceinline__ W RK1(int round, int kind, W v) {
+    return round ? round_kind<W>(kind, v) : v;
+}
+template <class W2>
+__device__ __forceinline__ W2 RKV(int round, int kind, W2 v) {
+    return round ? round_kind_v<W2>(kind, v) : v;
+}
+
 struct FusedArgs {
     Geo g;
     const void* qin;
@@ -230,12 +240,12 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             const WC Tv = O::div(O::mul(gM2, pr), rho);
             PT* pp = Pr + slot * TL::R4N + i;
             constexpr int FS = TL::NRING * TL::R4N;
-            pp[0] = cvt<PT>(round_kind<WC>(a.pc.kind[0], ux));
-            pp[FS] = cvt<PT>(round_kind<WC>(a.pc.kind[1], uy));
-            pp[2 * FS] = cvt<PT>(round_kind<WC>(a.pc.kind[2], uz));
-            pp[3 * FS] = cvt<PT>(round_kind<WC>(a.pc.kind[4], Tv));
+            pp[0] = cvt<PT>(RK1<WC>(a.pc.round, a.pc.kind[0], ux));
+            pp[FS] = cvt<PT>(RK1<WC>(a.pc.round, a.pc.kind[1], uy));
+            pp[2 * FS] = cvt<PT>(RK1<WC>(a.pc.round, a.pc.kind[2], uz));
+            pp[3 * FS] = cvt<PT>(RK1<WC>(a.pc.round, a.pc.kind[4], Tv));
             if (rx >= 2 && rx < TL::TX + 6 && ry >= 2 && ry < TL::TY + 6) {
-                Ppr[slot * TL::R2N + (ry - 2) * TL::R2X + (rx - 2)] = cvt<PT>(round_kind<WC>(a.pc.kind[3], pr));
+                Ppr[slot * TL::R2N + (ry - 2) * TL::R2X + (rx - 2)] = cvt<PT>(RK1<WC>(a.pc.round, a.pc.kind[3], pr));
                 T* qq = Qr + slot * TL::R2N + (ry - 2) * TL::R2X + (rx - 2);
                 constexpr int QF = TL::NRING * TL::R2N;
                 qq[0] = cvt<T>(q0);

@@ -208,13 +208,13 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
             const WC2 Tv = O::div(O::mul(gM2, pr), rho);
             constexpr int FS = TL::NRING * TL::R4N;
             PT* pp = Pr + slot * TL::R4N + ry * TL::R4X + rx;
-            stv<PT>(pp, cvt<PT2>(round_kind_v<WC2>(a.pc.kind[0], ux)));
-            stv<PT>(pp + FS, cvt<PT2>(round_kind_v<WC2>(a.pc.kind[1], uy)));
-            stv<PT>(pp + 2 * FS, cvt<PT2>(round_kind_v<WC2>(a.pc.kind[2], uz)));
-            stv<PT>(pp + 3 * FS, cvt<PT2>(round_kind_v<WC2>(a.pc.kind[4], Tv)));
+            stv<PT>(pp, cvt<PT2>(RKV<WC2>(a.pc.round, a.pc.kind[0], ux)));
+            stv<PT>(pp + FS, cvt<PT2>(RKV<WC2>(a.pc.round, a.pc.kind[1], uy)));
+            stv<PT>(pp + 2 * FS, cvt<PT2>(RKV<WC2>(a.pc.round, a.pc.kind[2], uz)));
+            stv<PT>(pp + 3 * FS, cvt<PT2>(RKV<WC2>(a.pc.round, a.pc.kind[4], Tv)));
             if (rx >= 2 && rx < TL::TX + 6 && ry >= 2 && ry < TL::TY + 6) {
                 const int q2i = (ry - 2) * TL::R2X + (rx - 2);
-                stv<PT>(Ppr + slot * TL::R2N + q2i, cvt<PT2>(round_kind_v<WC2>(a.pc.kind[3], pr)));
+                stv<PT>(Ppr + slot * TL::R2N + q2i, cvt<PT2>(RKV<WC2>(a.pc.round, a.pc.kind[3], pr)));
                 T* qq = Qr + slot * TL::R2N + q2i;
                 constexpr int QF = TL::NRING * TL::R2N;
                 stv<T>(qq, cvt<T2>(q0));

@@ -113,6 +113,7 @@ __device__ __forceinline__ GlobalAcc<T, QS, PT> make_acc(const Geo& g, const QS*
 struct PrimConsts {
     double half, gm1, gM2;
     int kind[5];  // storage kinds of u v w p T
+    int round;    // 0: every kind >= the primitives compute kind -> stores are exact
 };
 
 // primitives_impl (physics.cpp:281-331) at wk compute WC, over every Q plane

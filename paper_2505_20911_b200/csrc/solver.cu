@@ -406,7 +406,11 @@ PrimConsts Solver::prim_consts() const {
     pc.half = round_to(c, 0.5);
     pc.gm1 = round_to(c, gamma - 1.0);
     pc.gM2 = round_to(c, gamma * mach * mach);
-    for (int i = 0; i < 5; ++i) pc.kind[i] = kinds_prim[i];
+    pc.round = 0;
+    for (int i = 0; i < 5; ++i) {
+        pc.kind[i] = kinds_prim[i];
+        if (kinds_prim[i] < c) pc.round = 1;
+    }
     return pc;
 }
 ResConsts Solver::res_consts() const {
