@@ -26,6 +26,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
 
 METRIC = ("grid-pt updates/s per RK step (TGV 512^3, per precision mode) at 1/2/4/8 B200; "
           "% HBM roofline")
@@ -153,7 +154,7 @@ def run_reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": dtype_of(args.precision), "data": "synthetic",
-        "config": {"workload": f"TGV {args.n}^3 {args.precision}", "sample": sample},
+        "config": {"workload": f"TGV {args.grid}^3 {args.precision}", "sample": sample},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -174,7 +175,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--grid", type=int, default=512, help="n of the n^3 TGV grid")
     ap.add_argument("--precision", default="DP")
     ap.add_argument("--strategy", default="storesome")
     ap.add_argument("--emulation", default="strict")
@@ -185,6 +186,8 @@ def main():
                     help="extra precision modes measured after the headline (per_precision)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nccl", action="store_true",
+                    help="use the NCCL transport even on one rank (self-exchange)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -199,16 +202,17 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    use_nccl = world > 1 or args.nccl
+    if use_nccl:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     hbm, peak_src = peaks()
 
     def measure(preset, with_extras):
-        n = args.n
+        n = args.grid
         dt = DT.get(n, 2.5e-4)
         prec = m.resolve_preset(preset, args.emulation)
         decomp = None
-        if world > 1:
+        if use_nccl:
             obj = [m.Solver.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
             decomp = m.Decomposition(pz=world, mode=1, rank=rank, device=local, nccl_id=obj[0])
@@ -224,7 +228,7 @@ def main():
         stream = torch.cuda.ExternalStream(s.stream)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.profile(True)
-        if world > 1:
+        if use_nccl:
             dist.barrier()
         torch.cuda.synchronize()
         with ClockSampler(local) as clk:
@@ -234,7 +238,7 @@ def main():
             s.synchronize()
             torch.cuda.synchronize()
         ms_total = ev0.elapsed_time(ev1)
-        if world > 1:
+        if use_nccl:
             t = torch.tensor([ms_total], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_total = float(t.item())
@@ -293,10 +297,10 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": dtype_of(args.precision), "data": "synthetic",
-            "config": {"workload": f"TGV {args.n}^3 {args.precision} (M=0.1, Re=1600, "
+            "config": {"workload": f"TGV {args.grid}^3 {args.precision} (M=0.1, Re=1600, "
                                    f"{args.split}, {args.strategy}, {args.emulation})",
-                       "n": args.n, "precision": args.precision, "path": head["path"],
-                       "decomposition": f"z-slabs x{world}",
+                       "n": args.grid, "precision": args.precision, "path": head["path"],
+                       "decomposition": f"z-slabs x{world}" + (" (NCCL)" if use_nccl else ""),
                        "l2": "state >> 126 MB L2 (no flush needed)"},
             "roofline": head["roofline"],
             "b_alg": {"bytes_per_pt_per_step": head["b_alg_bytes_per_pt"],
@@ -319,7 +323,7 @@ def main():
             except Exception as e:
                 line["cpu_baseline"] = {"value": None, "error": str(e)}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_nccl:
         dist.destroy_process_group()
     return 0
 

@@ -45,12 +45,13 @@ static thread_local std::string g_err;
 
 // ---------------------------------------------------------------------------
 // NCCL, loaded on demand (only MPFD_DECOMP_NCCL needs it)
+struct NcclUniqueId {  // ncclUniqueId (nccl.h): passed by value
+    char internal[128];
+};
 struct Nccl {
-    typedef int (*GetUniqueId)(void*);
-    typedef int (*CommInitRank)(void**, int, const void* /*by value struct*/, int);
     void* lib = nullptr;
-    int (*getUniqueId)(void*) = nullptr;
-    int (*commInitRank)(void**, int, char[128], int) = nullptr;
+    int (*getUniqueId)(NcclUniqueId*) = nullptr;
+    int (*commInitRank)(void**, int, NcclUniqueId, int) = nullptr;
     int (*commDestroy)(void*) = nullptr;
     int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
     int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
@@ -70,8 +71,8 @@ struct Nccl {
                 if (!p) throw DeviceError(std::string("NCCL symbol missing: ") + s);
                 return p;
             };
-            n.getUniqueId = (int (*)(void*))sym("ncclGetUniqueId");
-            n.commInitRank = (int (*)(void**, int, char[128], int))sym("ncclCommInitRank");
+            n.getUniqueId = (int (*)(NcclUniqueId*))sym("ncclGetUniqueId");
+            n.commInitRank = (int (*)(void**, int, NcclUniqueId, int))sym("ncclCommInitRank");
             n.commDestroy = (int (*)(void*))sym("ncclCommDestroy");
             n.send = (int (*)(const void*, size_t, int, int, void*, cudaStream_t))sym("ncclSend");
             n.recv = (int (*)(void*, size_t, int, int, void*, cudaStream_t))sym("ncclRecv");
@@ -315,11 +316,11 @@ void Solver::setup(const mpfd_grid* grid, const mpfd_precision* p, int strategy_
         s.geo.plane = (long long)n * n;
         s.geo.planes = nz_local + 2 * kHalo;
     }
-    if (mode == MPFD_DECOMP_NCCL && pz > 1) {
+    if (mode == MPFD_DECOMP_NCCL) {
         if (!d.nccl_id) throw ConfigError("NCCL decomposition needs nccl_id");
         CK(cudaSetDevice(slabs[0].device));
-        char id[128];
-        std::memcpy(id, d.nccl_id, 128);
+        NcclUniqueId id;
+        std::memcpy(id.internal, d.nccl_id, 128);
         Nccl& nc = Nccl::get();
         nc.check(nc.commInitRank(&comm, pz, id, rank), "ncclCommInitRank");
     }
@@ -615,7 +616,7 @@ void Solver::init(int case_kind) {
 // H*5*ny*nx storage-precision values per direction.
 void Solver::halo_refresh() {
     const size_t bq = byte_width(plan.qk);
-    if (mode == MPFD_DECOMP_NCCL && pz > 1) {
+    if (mode == MPFD_DECOMP_NCCL) {
         Slab& s = slabs[0];
         CK(cudaSetDevice(s.device));
         const HaloPlan hp = halo_plan(n, pz, rank, (int)bq);
@@ -803,7 +804,7 @@ bool Solver::poll_div(bool block) {
         sync();
     }
     for (size_t i = 0; i < slabs.size(); ++i) any |= pinned_flag[i];
-    if (mode == MPFD_DECOMP_NCCL && pz > 1 && block) {
+    if (mode == MPFD_DECOMP_NCCL && block) {
         int* d = nullptr;
         Slab& s = slabs[0];
         CK(cudaMalloc(&d, sizeof(int)));
@@ -840,7 +841,7 @@ bool Solver::resolve_div(mpfd_divergence* ev, double dt) {
         for (int a = 0; a < 3; ++a)
             for (int b = 0; b < 5; ++b) tot.idx[a][b] = std::min(tot.idx[a][b], d.idx[a][b]);
     }
-    if (mode == MPFD_DECOMP_NCCL && pz > 1) {
+    if (mode == MPFD_DECOMP_NCCL) {
         // global min over ranks of (iteration, substep) and the index table
         unsigned long long buf[16];
         buf[0] = tot.flag ? (unsigned long long)tot.iter * 3 + tot.sub : ULLONG_MAX;
@@ -916,7 +917,7 @@ void Solver::diagnostics(int weighting, double t, int threads, mpfd_diag* out) {
             }
             CK(cudaStreamSynchronize(s.stream));
         }
-        if (mode == MPFD_DECOMP_NCCL && pz > 1) {
+        if (mode == MPFD_DECOMP_NCCL) {
             // gather every rank's parts in rank (= global z) order
             Slab& s = slabs[0];
             const size_t cnt = parts.size();
@@ -1017,7 +1018,9 @@ int mpfd_b200_split_preset(const char* name, mpfd_split* out) {
 int mpfd_b200_nccl_unique_id(void* out128) {
     return guard([&] {
         Nccl& nc = Nccl::get();
-        nc.check(nc.getUniqueId(out128), "ncclGetUniqueId");
+        NcclUniqueId id;
+        nc.check(nc.getUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out128, id.internal, 128);
         return MPFD_OK;
     });
 }
@@ -1189,7 +1192,7 @@ int mpfd_b200_advance(mpfd_solver* h, const mpfd_step* st, mpfd_diag* series, lo
         long done = 0;
         int status = MPFD_OK;
         mpfd_divergence e{};
-        const bool multi = S.mode == MPFD_DECOMP_NCCL && S.pz > 1;
+        const bool multi = S.mode == MPFD_DECOMP_NCCL;
         for (long it = 0; it < st->n_iterations; ++it) {
             const bool last = it + 1 == st->n_iterations;
             for (int sub = 0; sub < 3; ++sub)

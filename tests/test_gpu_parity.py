@@ -249,3 +249,34 @@ def test_paths_agree_64(b200, path, pz):
         s.advance(b200.StepConfig(0.002, 3, 0))
         c.advance(0.002, 3, 0)
         assert_state(s, c, (0, 1), f"{path} pz{pz} {preset}")
+
+
+def test_nccl_transport_single_rank(b200):
+    """The NCCL code path (dlopen, ncclCommInitRank, grouped send/recv of the
+    ghost planes, allgather of diagnostics partials, allreduce of the
+    divergence record) with one rank exchanging with itself: bitwise equal
+    to the LOCAL path."""
+    n = 32
+    ref = b200_solver(b200, n, "HPSP")
+    nid = b200.Solver.nccl_unique_id()
+    nc = b200_solver(b200, n, "HPSP", decomp=b200.Decomposition(pz=1, mode=1, rank=0, nccl_id=nid))
+    ref.init_tgv()
+    nc.init_tgv()
+    r1 = ref.advance(b200.StepConfig(0.002, 4, 2))
+    r2 = nc.advance(b200.StepConfig(0.002, 4, 2))
+    for cls in (0, 1):
+        for comp in range(5):
+            assert same_bits(ref.get_field(cls, comp), nc.get_field(cls, comp))
+    assert [(x.kinetic_energy, x.enstrophy) for x in r1.series] == \
+           [(x.kinetic_energy, x.enstrophy) for x in r2.series]
+    # divergence through the NCCL reduction of the event record
+    kw = dict(preset="DP", split="Divergence", viscous=False, mach=0.4)
+    a = b200_solver(b200, 16, **kw)
+    b = b200_solver(b200, 16, decomp=b200.Decomposition(pz=1, mode=1, rank=0,
+                                                        nccl_id=b200.Solver.nccl_unique_id()), **kw)
+    a.init_tgv()
+    b.init_tgv()
+    ra = a.advance(b200.StepConfig(0.2, 400, 10))
+    rb = b.advance(b200.StepConfig(0.2, 400, 10))
+    assert ra.diverged and rb.diverged and ra.divergence == rb.divergence
+    assert ra.iterations_run == rb.iterations_run

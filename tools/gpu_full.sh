@@ -7,9 +7,9 @@ timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $OUT/pytest_
 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1
 timeout 900 python bench.py ${BENCH_ARGS} > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
-   python bench.py --n 256 --steps 1 --warmup 3 --modes "" --no-e2e --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
+   python bench.py --grid 256 --steps 1 --warmup 3 --modes "" --no-e2e --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
 for P in ${NCU_PRESETS:-DP SPDP HPSP}; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fused -s 3 -c 1 \
-     -o $OUT/prof_$P python bench.py --n 256 --precision $P --steps 1 --warmup 3 --modes "" --no-e2e --no-cpu-baseline > $OUT/ncu_$P.log 2>&1
+     -o $OUT/prof_$P python bench.py --grid 256 --precision $P --steps 1 --warmup 3 --modes "" --no-e2e --no-cpu-baseline > $OUT/ncu_$P.log 2>&1
 done
 ls -la $OUT
