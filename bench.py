@@ -11,7 +11,10 @@ far larger than the 126 MB L2, so no explicit flush is needed between steps.
   python bench.py --impl reference ...     # the reference CPU implementation
 
 Multi-GPU: launched by torch.distributed.run, one rank per GPU; z-slab
-decomposition of the n^3 cube with NCCL halo exchange (strong scaling).
+decomposition with NCCL halo exchange overlapped with the interior planes.
+Default --scaling weak: every rank owns one n^3 period (the grid stacks N
+TGV periods along z, GridSpec.z_periods = N), so per-GPU work is fixed;
+--scaling strong splits one n^3 cube over the N ranks.
 """
 from __future__ import annotations
 
@@ -26,7 +29,10 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
+# keep stdout to the one JSON line: NCCL prints its version banner at
+# NCCL_DEBUG >= VERSION (WARN included), so the level stays unset (errors only)
+if os.environ.get("NCCL_DEBUG", "").upper() in ("VERSION", "WARN"):
+    del os.environ["NCCL_DEBUG"]
 
 METRIC = ("grid-pt updates/s per RK step (TGV 512^3, per precision mode) at 1/2/4/8 B200; "
           "% HBM roofline")
@@ -188,6 +194,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nccl", action="store_true",
                     help="use the NCCL transport even on one rank (self-exchange)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="exchange ghost planes before the substep instead of overlapping")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -204,6 +213,9 @@ def main():
     torch.cuda.set_device(local)
     use_nccl = world > 1 or args.nccl
     if use_nccl:
+        if "RANK" not in os.environ:  # --nccl without a launcher: a 1-rank group
+            os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=os.environ.get("MASTER_PORT", "29533"))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     hbm, peak_src = peaks()
 
@@ -218,10 +230,13 @@ def main():
             decomp = m.Decomposition(pz=world, mode=1, rank=rank, device=local, nccl_id=obj[0])
         else:
             decomp = m.Decomposition(device=local)
-        s = m.Solver(m.GridSpec(n), prec, args.strategy, m.FlowParams(0.1, 1600.0, 0.72, 1.4, True),
-                     args.split, decomp)
+        zper = world if args.scaling == "weak" else 1
+        s = m.Solver(m.GridSpec(n, z_periods=zper), prec, args.strategy,
+                     m.FlowParams(0.1, 1600.0, 0.72, 1.4, True), args.split, decomp)
         if args.path != "auto":
             s.set_path(args.path)
+        if args.no_overlap:
+            s.set_overlap(False)
         s.init_tgv()
         s.run_steps(args.warmup, dt)
         s.synchronize()
@@ -245,10 +260,11 @@ def main():
         kms, klaunch = s.profile_read()
         s.profile(False)
         ms_step = ms_total / args.steps
-        rate = n ** 3 / (ms_step * 1e-3)
+        npts = n ** 3 * zper  # whole job
+        rate = npts / (ms_step * 1e-3)
         # roofline of the dominant kernel (class 0: residual / fused step)
         bq, bt, br, bw = PRESET_KINDS[preset]
-        nloc = n ** 3 // world
+        nloc = npts // world
         fused = klaunch[1] == 0
         if fused:
             # compulsory per substep: read Q, write Q; Qt read (substeps 1,2) + write
@@ -257,7 +273,9 @@ def main():
         else:
             per_pt = 5 * bq + 5 * br
             kname = "staged residual (k_resid)"
-        avg_ms = kms[0] / max(1, klaunch[0])
+        # dominant-kernel time per substep (an overlapped substep is one
+        # interior + two boundary launches covering the slab once)
+        avg_ms = kms[0] / (3 * args.steps) if fused else kms[0] / max(1, klaunch[0])
         achieved = per_pt * nloc / (avg_ms * 1e-3) / 1e9
         res = {
             "preset": preset, "value": rate, "ms_per_step": ms_step,
@@ -265,7 +283,7 @@ def main():
             "b_alg_frac": rate * b_alg(preset) / 1e9 / hbm,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic_lookup(preset, n, fused),
-                         "kernel": kname, "avg_launch_ms": avg_ms,
+                         "kernel": kname, "avg_ms_per_substep": avg_ms,
                          "bytes_per_pt_per_launch": per_pt, "peak_source": peak_src},
             "kernel_ms": {"dominant": kms[0], "rk": kms[1], "halo": kms[2], "other": kms[3]},
             "gpu_launches": int(klaunch[0] + klaunch[1] + klaunch[3]),
@@ -295,12 +313,19 @@ def main():
         line = {
             "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
-            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": dtype_of(args.precision), "data": "synthetic",
-            "config": {"workload": f"TGV {args.grid}^3 {args.precision} (M=0.1, Re=1600, "
-                                   f"{args.split}, {args.strategy}, {args.emulation})",
+            "config": {"workload": (f"TGV {args.grid}^3 {args.precision} (M=0.1, Re=1600, "
+                                    f"{args.split}, {args.strategy}, {args.emulation})"
+                                    + (f", {args.grid}^3 per GPU ({args.grid}x{args.grid}x"
+                                       f"{args.grid * world} stacked periods)"
+                                       if args.scaling == "weak" and world > 1 else "")),
                        "n": args.grid, "precision": args.precision, "path": head["path"],
                        "decomposition": f"z-slabs x{world}" + (" (NCCL)" if use_nccl else ""),
+                       "halo_exchange": ("overlapped with interior planes (2 streams)"
+                                         if use_nccl and not args.no_overlap else
+                                         "before each substep" if use_nccl else
+                                         "periodic self-copy (1 slab)"),
                        "l2": "state >> 126 MB L2 (no flush needed)"},
             "roofline": head["roofline"],
             "b_alg": {"bytes_per_pt_per_step": head["b_alg_bytes_per_pt"],

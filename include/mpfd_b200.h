@@ -43,10 +43,16 @@ enum { MPFD_KE_PLAIN = 0, MPFD_KE_DENSITY = 1 };
 /* decomposition transport */
 enum { MPFD_DECOMP_LOCAL = 0, MPFD_DECOMP_NCCL = 1 };
 
-/* GridSpec (field.hpp:20-56): cube n^3, spacing domain_length/n, halo 4. */
+/* GridSpec (field.hpp:20-56): cube n^3, spacing domain_length/n, halo 4.
+ * z_periods > 1 (B200 extension for weak scaling, SURVEY.md 7 hard part 6)
+ * stacks that many periods along z: n x n x (z_periods*n) points, z length
+ * z_periods*domain_length; the TGV initial condition repeats exactly
+ * (plane k takes the values of plane k mod n).  0 or 1: the reference cube.
+ * State carriers then span (z_periods*n + 8) planes of (n+8)^2. */
 typedef struct {
     int n;
     double domain_length; /* 0 -> 2*pi */
+    int z_periods;        /* 0/1: cube */
 } mpfd_grid;
 
 /* PrecisionConfig (precision.hpp:181-193) with custom_overrides as parallel
@@ -193,6 +199,12 @@ int mpfd_b200_halo_plan(int n, int pz, int rank, int bytes_q, long long out[9]);
 
 /* Which residual path runs: 0 = staged multi-kernel, 1 = fused. */
 int mpfd_b200_set_path(mpfd_solver* s, int path);
+/* Overlap of the z-halo exchange with the interior planes (fused path,
+ * pz > 1 or NCCL): 1 (default) splits each substep into the interior
+ * launch, which runs while the ghost planes are exchanged on a second
+ * stream, and the boundary launches after it; 0 exchanges first.  Results
+ * are bitwise identical either way. */
+int mpfd_b200_set_overlap(mpfd_solver* s, int enable);
 
 #ifdef __cplusplus
 }

@@ -74,7 +74,7 @@ class Solver {
   public:
     Solver(int n, const mpfd_precision& prec, int strategy, const mpfd_flow& flow, const mpfd_split& split,
            const mpfd_decomp* decomp = nullptr) {
-        const mpfd_grid g{n, 0.0};
+        const mpfd_grid g{n, 0.0, 1};
         check(mpfd_b200_create(&g, &prec, strategy, &flow, &split, decomp, &s_));
     }
     ~Solver() {

@@ -50,7 +50,8 @@ struct FusedArgs {
     StageConsts sc;
     RkConsts kc;
     int write_r;
-    int lz;  // z planes per CTA
+    int lz;        // z planes per CTA
+    int zlo, zhi;  // local output planes [zlo, zhi) of this launch
     DevDiv* div;
     int iter, sub;
 };
@@ -145,7 +146,10 @@ __device__ __forceinline__ void rk_point(const FusedArgs& a, int comp, int c, lo
 template <class QS, class TS, class RS, class PT, class WC, class T, class TC, class QC, bool STAGED, class TL,
           int MINB, unsigned SPL>
 __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
-    if (a.div->flag) return;
+    // a substep after a divergence is a no-op; launches of the substep that
+    // diverged (interior and boundary of an overlapped substep) all run, so
+    // the first point in scan order is found
+    if (a.div->flag && (a.div->iter != a.iter || a.div->sub != a.sub)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using SM = FusedSmem<TL, T, PT>;
     PT* Pr = (PT*)smem_raw;
@@ -157,8 +161,8 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
     const int tid = threadIdx.x;
     const int tx = tid % TL::TX, ty = tid / TL::TX;
     const int x0 = blockIdx.x * TL::TX, y0 = blockIdx.y * TL::TY;
-    const int zs = blockIdx.z * a.lz;
-    const int ze = min(zs + a.lz, g.nzl);
+    const int zs = a.zlo + blockIdx.z * a.lz;
+    const int ze = min(zs + a.lz, a.zhi);
     const int x = x0 + tx, y = y0 + ty;
     const bool own = x < g.nx && y < g.ny;
     const long long o = own ? (long long)y * g.nx + x : 0;

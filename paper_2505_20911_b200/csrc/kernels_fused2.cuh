@@ -112,7 +112,10 @@ __device__ __forceinline__ void rk_pair(const FusedArgs& a, int comp, int c, lon
 template <class QS, class TS, class RS, class PT, class WC, class T, class TC, class QC, bool STAGED, class TL,
           int MINB, unsigned SPL>
 __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
-    if (a.div->flag) return;
+    // a substep after a divergence is a no-op; launches of the substep that
+    // diverged (interior and boundary of an overlapped substep) all run, so
+    // the first point in scan order is found
+    if (a.div->flag && (a.div->iter != a.iter || a.div->sub != a.sub)) return;
     using T2 = typename V2<T>::type;
     using WC2 = typename V2<WC>::type;
     using PT2 = typename V2<PT>::type;
@@ -132,8 +135,8 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
     const int tid = threadIdx.x;
     const int tx = tid % TXP, ty = tid / TXP;
     const int x0 = blockIdx.x * TL::TX, y0 = blockIdx.y * TL::TY;
-    const int zs = blockIdx.z * a.lz;
-    const int ze = min(zs + a.lz, g.nzl);
+    const int zs = a.zlo + blockIdx.z * a.lz;
+    const int ze = min(zs + a.lz, a.zhi);
     const int x = x0 + 2 * tx, y = y0 + ty;
     const bool own = x < g.nx && y < g.ny;
     const long long o = own ? (long long)y * g.nx + x : 0;
@@ -392,13 +395,13 @@ struct FusedPlan {
     using TL2 = Tile<64, 8>;
     static constexpr int MINB2 = (sizeof(T) == 2 && sizeof(PT) == 2) ? 2 : 1;
 
-    static int z_range(const Geo& g, int tx, int ty, int minb) {
+    static int z_range(const Geo& g, int nz, int tx, int ty, int minb) {
         // z planes per CTA: about 8 waves of CTAs over the 148 SMs, but at
         // least 16 planes so the 8-plane start-up of each CTA stays small
         const long long cols = (long long)((g.nx + tx - 1) / tx) * ((g.ny + ty - 1) / ty);
         const int nzs = (int)std::max<long long>(1, (148LL * minb * 8 + cols - 1) / cols);
-        int lz = (g.nzl + nzs - 1) / nzs;
-        return std::max(lz, std::min(16, g.nzl));
+        int lz = (nz + nzs - 1) / nzs;
+        return std::max(lz, std::min(16, nz));
     }
 
     template <bool ST, unsigned SPL>
@@ -412,9 +415,9 @@ struct FusedPlan {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 attr = true;
             }
-            a.lz = z_range(a.g, TL2::TX, TL2::TY, MINB2);
+            a.lz = z_range(a.g, a.zhi - a.zlo, TL2::TX, TL2::TY, MINB2);
             const dim3 grid((a.g.nx + TL2::TX - 1) / TL2::TX, (a.g.ny + TL2::TY - 1) / TL2::TY,
-                            (a.g.nzl + a.lz - 1) / a.lz);
+                            (a.zhi - a.zlo + a.lz - 1) / a.lz);
             kern<<<grid, TL2::NT / 2, smem, st>>>(a);
             return;
             }
@@ -426,17 +429,19 @@ struct FusedPlan {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             attr = true;
         }
-        a.lz = z_range(a.g, TL::TX, TL::TY, FT::MINB);
+        a.lz = z_range(a.g, a.zhi - a.zlo, TL::TX, TL::TY, FT::MINB);
         const dim3 grid((a.g.nx + TL::TX - 1) / TL::TX, (a.g.ny + TL::TY - 1) / TL::TY,
-                        (a.g.nzl + a.lz - 1) / a.lz);
+                        (a.zhi - a.zlo + a.lz - 1) / a.lz);
         kern<<<grid, TL::NT, smem, st>>>(a);
     }
 
     static void launch(const Geo& g, cudaStream_t st, const void* qin, void* qout, const void* qtin, void* qtout,
                        void* r, const PrimConsts& pc, const ResConsts& rc, const StageConsts& sc, bool staged,
-                       const RkConsts& kc, bool write_r, DevDiv* div, int iter, int sub) {
+                       const RkConsts& kc, bool write_r, DevDiv* div, int iter, int sub, int zlo, int zhi) {
         FusedArgs a;
         a.g = g;
+        a.zlo = zlo;
+        a.zhi = zhi;
         a.qin = qin;
         a.qout = qout;
         a.qtin = qtin;

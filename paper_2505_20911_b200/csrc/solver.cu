@@ -110,11 +110,11 @@ struct HaloPlan {
     long long send_up, recv_lo, send_dn, recv_hi, block;
     int up, dn, z0, nzl;
 };
-static HaloPlan halo_plan(int n, int pz, int rank, int bq) {
-    if (pz < 1 || n % pz != 0) throw ConfigError("grid n is not divisible by the z process count");
+static HaloPlan halo_plan(int n, int nz, int pz, int rank, int bq) {
+    if (pz < 1 || nz % pz != 0) throw ConfigError("grid nz is not divisible by the z process count");
     if (rank < 0 || rank >= pz) throw ConfigError("rank out of range");
     HaloPlan p;
-    p.nzl = n / pz;
+    p.nzl = nz / pz;
     if (p.nzl < kHalo) throw ConfigError("z slab thinner than the halo depth (4)");
     const long long plane5 = 5LL * n * n * bq;
     p.block = kHalo * plane5;
@@ -151,6 +151,7 @@ static double tree_of_chunks(const double* c, size_t n) {
 struct Solver {
     // configuration
     int n = 0;
+    int zper = 1, nzg = 0;  // z periods (weak scaling) and global z planes n * zper
     double L = 0.0, h = 0.0;
     Precision prec;
     int strategy = 0;
@@ -198,6 +199,13 @@ struct Solver {
     void upload_slab(Slab& s, int cls, int comp, const double* src, size_t ld_row, size_t ld_plane);
     void get_interior(int cls, int comp, double* dst, size_t ld_row, size_t ld_plane, int off);
     void halo_refresh();
+    // overlapped exchange (fused path): off for one slab per process with
+    // pz == 1 in LOCAL mode (no neighbour) or slabs too thin to split
+    int overlap = 1;
+    bool overlap_ok() const {
+        return overlap && use_fused() && (pz > 1 || mode == MPFD_DECOMP_NCCL) && nzl() >= 3 * kHalo;
+    }
+    void exchange_async();
     void residual_enqueue(int iter, int sub);
     void rk_enqueue(int sub, const double a[3], const double b[3], double dt, int iter);
     void substep_enqueue(int sub, const double a[3], const double b[3], double dt, int iter, bool write_r);
@@ -206,7 +214,7 @@ struct Solver {
     void diagnostics(int weighting, double t, int threads, mpfd_diag* out);
     void sync();
     template <class F>
-    void timed(int cls, const Slab& s, F&& f);
+    void timed(int cls, const Slab& s, F&& f, int launches = 1);
     void begin_profile_window();
     void flush_profile();
 };
@@ -220,6 +228,9 @@ Solver::~Solver() {
         cudaFree(s.div);
         cudaFree(s.staging);
         if (s.stream) cudaStreamDestroy(s.stream);
+        if (s.comm) cudaStreamDestroy(s.comm);
+        if (s.ev_x) cudaEventDestroy(s.ev_x);
+        if (s.ev_b) cudaEventDestroy(s.ev_b);
     }
     for (auto& v : prof_ev)
         for (auto& e : v) {
@@ -235,6 +246,8 @@ void Solver::setup(const mpfd_grid* grid, const mpfd_precision* p, int strategy_
     if (!grid || !p || !flow || !sp) throw ConfigError("null configuration pointer");
     n = grid->n;
     if (n < 5) throw ConfigError("GridSpec: n must be >= 5");
+    zper = grid->z_periods > 0 ? grid->z_periods : 1;
+    nzg = n * zper;
     L = grid->domain_length > 0 ? grid->domain_length : 2.0 * 3.14159265358979323846;
     h = L / n;
     prec.q = p->q_vector;
@@ -300,9 +313,9 @@ void Solver::setup(const mpfd_grid* grid, const mpfd_precision* p, int strategy_
     pz = d.pz < 1 ? 1 : d.pz;
     mode = d.mode;
     rank = d.rank;
-    if (n % pz != 0) throw ConfigError("grid n is not divisible by the z process count");
-    if (n / pz < kHalo) throw ConfigError("z slab thinner than the halo depth (4)");
-    const int nz_local = n / pz;
+    if (nzg % pz != 0) throw ConfigError("grid nz is not divisible by the z process count");
+    if (nzg / pz < kHalo) throw ConfigError("z slab thinner than the halo depth (4)");
+    const int nz_local = nzg / pz;
     const int nslab = mode == MPFD_DECOMP_NCCL ? 1 : pz;
     slabs.resize(nslab);
     for (int i = 0; i < nslab; ++i) {
@@ -334,6 +347,9 @@ void Solver::alloc() {
     for (auto& s : slabs) {
         CK(cudaSetDevice(s.device));
         CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&s.comm, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&s.ev_x, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&s.ev_b, cudaEventDisableTiming));
         const size_t pl = (size_t)s.geo.plane;
         const size_t qel = (size_t)s.geo.planes * 5 * pl;
         const size_t iel = (size_t)s.geo.nzl * 5 * pl;
@@ -395,6 +411,7 @@ void Solver::reset_div() {
 void Solver::sync() {
     for (auto& s : slabs) {
         CK(cudaSetDevice(s.device));
+        CK(cudaStreamSynchronize(s.comm));
         CK(cudaStreamSynchronize(s.stream));
     }
 }
@@ -561,7 +578,9 @@ void Solver::init(int case_kind) {
         for (auto& v : f) v.assign(nzl_ * pl, 0.0);
         auto fill_planes = [&](size_t k0, size_t k1) {
             for (size_t k = k0; k < k1; ++k) {
-                const double z = (double)(z0 + k) * h_;
+                // z periods > 1 (weak scaling) repeat the 2 pi-periodic
+                // field: plane k takes the values of plane k mod n exactly
+                const double z = (double)((z0 + k) % (size_t)n) * h_;
                 for (int j = 0; j < n; ++j) {
                     const double y = j * h_;
                     for (int i = 0; i < n; ++i) {
@@ -619,7 +638,7 @@ void Solver::halo_refresh() {
     if (mode == MPFD_DECOMP_NCCL) {
         Slab& s = slabs[0];
         CK(cudaSetDevice(s.device));
-        const HaloPlan hp = halo_plan(n, pz, rank, (int)bq);
+        const HaloPlan hp = halo_plan(n, nzg, pz, rank, (int)bq);
         char* q = (char*)qcur(s);
         const size_t blk = (size_t)hp.block;
         const int up = hp.up, dn = hp.dn;
@@ -695,11 +714,65 @@ void Solver::halo_refresh() {
     halo_fresh = true;
 }
 
+// The z exchange of the current state's ghost planes, enqueued on each slab's
+// comm stream so it overlaps the interior planes of the next substep (SURVEY
+// 8(e)).  It reads the sending slabs' boundary planes, which the previous
+// substep's boundary launches wrote (ev_b), and writes only ghost planes,
+// which no interior launch reads.  ev_x marks it done for the boundary
+// launches.
+void Solver::exchange_async() {
+    const size_t bq = byte_width(plan.qk);
+    const int ns = (int)slabs.size();
+    // everything enqueued so far on each slab (the previous substep's
+    // launches, uploads) precedes the exchange
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        CK(cudaEventRecord(s.ev_b, s.stream));
+    }
+    if (mode == MPFD_DECOMP_NCCL) {
+        Slab& s = slabs[0];
+        CK(cudaSetDevice(s.device));
+        CK(cudaStreamWaitEvent(s.comm, s.ev_b, 0));
+        const HaloPlan hp = halo_plan(n, nzg, pz, rank, (int)bq);
+        char* q = (char*)qcur(s);
+        const size_t blk = (size_t)hp.block;
+        Nccl& nc = Nccl::get();
+        nc.check(nc.groupStart(), "ncclGroupStart");
+        nc.check(nc.send(q + hp.send_up, blk, 1, hp.up, comm, s.comm), "ncclSend");
+        nc.check(nc.recv(q + hp.recv_lo, blk, 1, hp.dn, comm, s.comm), "ncclRecv");
+        nc.check(nc.send(q + hp.send_dn, blk, 1, hp.dn, comm, s.comm), "ncclSend");
+        nc.check(nc.recv(q + hp.recv_hi, blk, 1, hp.up, comm, s.comm), "ncclRecv");
+        nc.check(nc.groupEnd(), "ncclGroupEnd");
+        ++prof_launch[2];
+        CK(cudaEventRecord(s.ev_x, s.comm));
+        return;
+    }
+    for (int i = 0; i < ns; ++i) {
+        Slab& s = slabs[i];
+        const Slab& prv = slabs[(i + ns - 1) % ns];
+        const Slab& nxt = slabs[(i + 1) % ns];
+        CK(cudaSetDevice(s.device));
+        CK(cudaStreamWaitEvent(s.comm, s.ev_b, 0));
+        CK(cudaStreamWaitEvent(s.comm, prv.ev_b, 0));
+        CK(cudaStreamWaitEvent(s.comm, nxt.ev_b, 0));
+        const size_t blk = (size_t)kHalo * 5 * s.geo.plane * bq;
+        char* q = (char*)qcur(s);
+        const char* pq = (const char*)qcur(prv);
+        const char* nq = (const char*)qcur(nxt);
+        CK(cudaMemcpyPeerAsync(q, s.device, pq + (size_t)prv.geo.nzl * 5 * prv.geo.plane * bq, prv.device, blk,
+                               s.comm));
+        CK(cudaMemcpyPeerAsync(q + (size_t)(s.geo.nzl + kHalo) * 5 * s.geo.plane * bq, s.device, nq + blk,
+                               nxt.device, blk, s.comm));
+        ++prof_launch[2];
+        CK(cudaEventRecord(s.ev_x, s.comm));
+    }
+}
+
 template <class F>
-void Solver::timed(int cls, const Slab& s, F&& f) {
+void Solver::timed(int cls, const Slab& s, F&& f, int launches) {
     if (!profiling) {
         f();
-        ++prof_launch[cls];
+        prof_launch[cls] += launches;
         return;
     }
     cudaEvent_t a, b;
@@ -709,7 +782,7 @@ void Solver::timed(int cls, const Slab& s, F&& f) {
     f();
     CK(cudaEventRecord(b, s.stream));
     prof_ev[cls].push_back({a, b});
-    ++prof_launch[cls];
+    prof_launch[cls] += launches;
 }
 
 void Solver::flush_profile() {
@@ -761,6 +834,39 @@ void Solver::rk_enqueue(int sub, const double a[3], const double b[3], double dt
 // one substep of advance's inner loop: evaluate -> rk_substep -> halo fill
 void Solver::substep_enqueue(int sub, const double a[3], const double b[3], double dt, int iter,
                              bool write_r) {
+    if (overlap_ok()) {
+        // interior planes [H, nzl-H) need no ghost plane: they run while the
+        // exchange is in flight; the 2H boundary planes follow it
+        const bool need_x = !halo_fresh;
+        if (need_x) exchange_async();
+        const PrimConsts pc = prim_consts();
+        const ResConsts rc = res_consts();
+        const StageConsts sc = stage_consts();
+        const RkConsts kc = rk_consts(sub, a, b, dt);
+        const bool staged = strategy == MPFD_DEFAULT && viscous;
+        for (auto& s : slabs) {
+            CK(cudaSetDevice(s.device));
+            const void* qin = qbuf ? s.q2 : s.q;
+            void* qout = qbuf ? s.q : s.q2;
+            const void* qtin = qbuf ? s.qt2 : s.qt;
+            void* qtout = qbuf ? s.qt : s.qt2;
+            const int nz = s.geo.nzl;
+            timed(0, s, [&] {
+                launch->fused(s, qin, qout, qtin, qtout, pc, rc, sc, staged, kc, write_r, iter, sub, kHalo,
+                              nz - kHalo);
+            });
+            if (need_x) CK(cudaStreamWaitEvent(s.stream, s.ev_x, 0));
+            timed(0, s, [&] {
+                launch->fused(s, qin, qout, qtin, qtout, pc, rc, sc, staged, kc, write_r, iter, sub, 0, kHalo);
+                launch->fused(s, qin, qout, qtin, qtout, pc, rc, sc, staged, kc, write_r, iter, sub, nz - kHalo,
+                              nz);
+            }, 2);
+            CK(cudaGetLastError());
+        }
+        qbuf ^= 1;
+        halo_fresh = false;
+        return;
+    }
     if (!halo_fresh) halo_refresh();
     if (use_fused()) {
         const PrimConsts pc = prim_consts();
@@ -775,7 +881,8 @@ void Solver::substep_enqueue(int sub, const double a[3], const double b[3], doub
             const void* qtin = qbuf ? s.qt2 : s.qt;
             void* qtout = qbuf ? s.qt : s.qt2;
             timed(0, s, [&] {
-                launch->fused(s, qin, qout, qtin, qtout, pc, rc, sc, staged, kc, write_r, iter, sub);
+                launch->fused(s, qin, qout, qtin, qtout, pc, rc, sc, staged, kc, write_r, iter, sub, 0,
+                              s.geo.nzl);
             });
             CK(cudaGetLastError());
         }
@@ -887,7 +994,7 @@ bool Solver::resolve_div(mpfd_divergence* ev, double dt) {
 // deterministic_sum tree shape (threads == 1: pure pairwise; > 1: 4096-chunked)
 void Solver::diagnostics(int weighting, double t, int threads, mpfd_diag* out) {
     if (!halo_fresh) halo_refresh();
-    const size_t N = (size_t)n * n * n;
+    const size_t N = (size_t)n * n * nzg;
     const size_t nch_total = N / 4096;
     bool aligned = ((size_t)nzl() * n * n) % 4096 == 0 && N >= 4096;
     if (aligned && threads <= 1 && (nch_total & (nch_total - 1)) != 0) aligned = false;
@@ -952,7 +1059,7 @@ void Solver::diagnostics(int weighting, double t, int threads, mpfd_diag* out) {
         sums[which] = sum;
     }
     const double cell = h * h * h;
-    const double vol = L * L * L;
+    const double vol = L * L * L * zper;
     out->t = t;
     out->kinetic_energy = sums[0] * cell / vol;
     out->enstrophy = sums[1] * cell / vol;
@@ -1059,7 +1166,7 @@ int mpfd_b200_init_uniform(mpfd_solver* s) {
 
 int mpfd_b200_set_state(mpfd_solver* s, int cls, int comp, const double* ext3) {
     return guard([&] {
-        const size_t e = (size_t)s->s.n + 8;
+        const size_t e = (size_t)s->s.n + 8;  // x, y extent; z extent nzg + 8
         s->s.set_interior(cls, comp, ext3, e, e * e, (int)((4 * e + 4) * e + 4));
         s->s.reset_div();
         return MPFD_OK;
@@ -1068,12 +1175,13 @@ int mpfd_b200_set_state(mpfd_solver* s, int cls, int comp, const double* ext3) {
 int mpfd_b200_get_state(mpfd_solver* s, int cls, int comp, double* ext3) {
     return guard([&] {
         const int n = s->s.n;
+        const size_t nz = (size_t)s->s.nzg;
         const size_t e = (size_t)n + 8;
         s->s.get_interior(cls, comp, ext3, e, e * e, (int)((4 * e + 4) * e + 4));
         // periodic halos (fill_halos_periodic, field.cpp:9-48) for Q; the
         // reference never fills Qt/R halos, which stay zero
         if (cls == 0) {
-            for (size_t kk = 4; kk < (size_t)n + 4; ++kk)
+            for (size_t kk = 4; kk < nz + 4; ++kk)
                 for (size_t jj = 4; jj < (size_t)n + 4; ++jj) {
                     double* row = ext3 + (kk * e + jj) * e;
                     for (int hh = 0; hh < 4; ++hh) {
@@ -1081,7 +1189,7 @@ int mpfd_b200_get_state(mpfd_solver* s, int cls, int comp, double* ext3) {
                         row[4 + n + hh] = row[4 + hh];
                     }
                 }
-            for (size_t kk = 4; kk < (size_t)n + 4; ++kk) {
+            for (size_t kk = 4; kk < nz + 4; ++kk) {
                 double* pl = ext3 + kk * e * e;
                 for (int hh = 0; hh < 4; ++hh) {
                     std::memcpy(pl + hh * e, pl + (hh + n) * e, e * sizeof(double));
@@ -1089,8 +1197,8 @@ int mpfd_b200_get_state(mpfd_solver* s, int cls, int comp, double* ext3) {
                 }
             }
             for (int hh = 0; hh < 4; ++hh) {
-                std::memcpy(ext3 + hh * e * e, ext3 + (hh + n) * e * e, e * e * sizeof(double));
-                std::memcpy(ext3 + (4 + n + hh) * e * e, ext3 + (4 + hh) * e * e, e * e * sizeof(double));
+                std::memcpy(ext3 + hh * e * e, ext3 + (hh + nz) * e * e, e * e * sizeof(double));
+                std::memcpy(ext3 + (4 + nz + hh) * e * e, ext3 + (4 + hh) * e * e, e * e * sizeof(double));
             }
         }
         return MPFD_OK;
@@ -1286,7 +1394,7 @@ int mpfd_b200_memory(mpfd_solver* h, size_t* device_bytes, size_t* census, size_
         if (device_bytes) *device_bytes = b;
         // memory_report over make_solver_fields' set (registry.cpp:24-39)
         const size_t e = (size_t)S.n + 8;
-        const size_t pts = e * e * e;
+        const size_t pts = e * e * ((size_t)S.nzg + 8);
         size_t tot = 0, cnt = 0;
         for (int c = 0; c < 5; ++c) {
             tot += pts * byte_width(S.prec.resolve(0, kQNames[c]));
@@ -1308,9 +1416,17 @@ int mpfd_b200_memory(mpfd_solver* h, size_t* device_bytes, size_t* census, size_
 
 int mpfd_b200_halo_plan(int n, int pz, int rank, int bytes_q, long long out[9]) {
     return guard([&] {
-        const HaloPlan p = halo_plan(n, pz, rank, bytes_q);
+        const HaloPlan p = halo_plan(n, n, pz, rank, bytes_q);
         const long long v[9] = {p.send_up, p.recv_lo, p.send_dn, p.recv_hi, p.block, p.up, p.dn, p.z0, p.nzl};
         for (int i = 0; i < 9; ++i) out[i] = v[i];
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_set_overlap(mpfd_solver* h, int enable) {
+    return guard([&] {
+        h->s.sync();
+        h->s.overlap = enable != 0;
         return MPFD_OK;
     });
 }

@@ -45,7 +45,7 @@ class DeviceError(RuntimeError):
 # ---------------------------------------------------------------------------
 # C structs (include/mpfd_b200.h)
 class _Grid(C.Structure):
-    _fields_ = [("n", C.c_int), ("domain_length", C.c_double)]
+    _fields_ = [("n", C.c_int), ("domain_length", C.c_double), ("z_periods", C.c_int)]
 
 
 class _Prec(C.Structure):
@@ -129,6 +129,7 @@ def lib():
         L.mpfd_b200_memory.argtypes = [P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
                                        C.POINTER(C.c_size_t)]
         L.mpfd_b200_set_path.argtypes = [P, I]
+        L.mpfd_b200_set_overlap.argtypes = [P, I]
         _lib = L
     return _lib
 
@@ -170,14 +171,24 @@ def resolve_preset(name: str, emulation: str | int = STRICT) -> PrecisionConfig:
 
 @dataclass
 class GridSpec:
+    """GridSpec (field.hpp:20-56).  z_periods > 1 is a B200 extension for weak
+    scaling: n x n x (z_periods*n) points, the 2 pi-periodic TGV repeated
+    exactly along z (include/mpfd_b200.h)."""
     n: int = 32
     domain_length: float = 2.0 * math.pi
+    z_periods: int = 1
 
     halo_depth = 4
 
     def __post_init__(self):
         if self.n < 5:
             raise ConfigError("GridSpec: n must be >= 5")
+        if self.z_periods < 1:
+            raise ConfigError("GridSpec: z_periods must be >= 1")
+
+    @property
+    def nz(self) -> int:
+        return self.n * self.z_periods
 
     def spacing(self) -> float:
         return self.domain_length / self.n
@@ -292,13 +303,14 @@ class Solver:
             split = split_preset(split)
         self.grid, self.precision, self.flow, self.split = grid, precision, flow, split
         self.n = grid.n
+        self.nz = grid.nz
         names = list(precision.custom_overrides)
         self._keep = [n.encode() for n in names]
         p = _Prec(precision.q_vector, precision.rk_arrays, precision.residuals,
                   precision.wk_arrays, precision.emulation, len(names),
                   (C.c_char_p * max(1, len(names)))(*self._keep),
                   (C.c_int * max(1, len(names)))(*[precision.custom_overrides[k] for k in names]))
-        g = _Grid(grid.n, grid.domain_length)
+        g = _Grid(grid.n, grid.domain_length, grid.z_periods)
         f = _Flow(flow.mach, flow.reynolds, flow.prandtl, flow.gamma, 1 if flow.viscous else 0)
         s = _Split(*(getattr(split, k) for k, _ in _Split._fields_))
         d = decomp or Decomposition()
@@ -339,12 +351,14 @@ class Solver:
     # --- carriers ----------------------------------------------------------
     def get_field(self, cls: int, comp: int) -> np.ndarray:
         """Interior n^3 binary64 carrier, indexed [k, j, i]."""
-        out = np.empty((self.n,) * 3)
+        out = np.empty((self.nz, self.n, self.n))
         _check(self.L.mpfd_b200_get_state_interior(self.h, cls, comp, _dp(out)))
         return out
 
     def set_field(self, cls: int, comp: int, arr: np.ndarray):
         a = np.ascontiguousarray(arr, dtype=np.float64)
+        if a.shape != (self.nz, self.n, self.n):
+            raise ConfigError(f"carrier shape {a.shape} != {(self.nz, self.n, self.n)}")
         _check(self.L.mpfd_b200_set_state_interior(self.h, cls, comp, _dp(a)))
 
     def get_state(self, cls: int) -> np.ndarray:
@@ -356,12 +370,15 @@ class Solver:
 
     def get_field_ext(self, cls: int, comp: int) -> np.ndarray:
         e = self.n + 8
-        out = np.zeros((e, e, e))
+        out = np.zeros((self.nz + 8, e, e))
         _check(self.L.mpfd_b200_get_state(self.h, cls, comp, _dp(out)))
         return out
 
     def set_field_ext(self, cls: int, comp: int, arr: np.ndarray):
         a = np.ascontiguousarray(arr, dtype=np.float64)
+        e = self.n + 8
+        if a.shape != (self.nz + 8, e, e):
+            raise ConfigError(f"carrier shape {a.shape} != {(self.nz + 8, e, e)}")
         _check(self.L.mpfd_b200_set_state(self.h, cls, comp, _dp(a)))
 
     # --- hot path ----------------------------------------------------------
@@ -437,3 +454,8 @@ class Solver:
 
     def set_path(self, path: str):
         _check(self.L.mpfd_b200_set_path(self.h, 1 if path == "fused" else 0))
+
+    def set_overlap(self, enable: bool):
+        """Overlap the z-halo exchange with the interior planes (default on;
+        bitwise identical results either way)."""
+        _check(self.L.mpfd_b200_set_overlap(self.h, 1 if enable else 0))

@@ -205,6 +205,58 @@ def test_local_slabs_bitwise(b200, pz):
     assert a == b
 
 
+@pytest.mark.parametrize("pz", [2, 3, 4])
+@pytest.mark.parametrize("preset", ["DP", "HPSP"])
+def test_overlapped_exchange_bitwise(b200, preset, pz):
+    """Interior launch overlapped with the ghost-plane exchange, boundary
+    launches after it: bitwise equal to the exchange-first schedule and to
+    one slab, state and diagnostics series."""
+    n = 48
+    one = b200_solver(b200, n, preset)
+    ov = b200_solver(b200, n, preset, decomp=b200.Decomposition(pz=pz))
+    seq = b200_solver(b200, n, preset, decomp=b200.Decomposition(pz=pz))
+    seq.set_overlap(False)
+    runs = []
+    for s in (one, ov, seq):
+        s.init_tgv()
+        runs.append(s.advance(b200.StepConfig(0.002, 5, 2)))
+    for cls in (0, 1):
+        for comp in range(5):
+            a = one.get_field(cls, comp)
+            assert same_bits(a, ov.get_field(cls, comp)), (cls, comp)
+            assert same_bits(a, seq.get_field(cls, comp)), (cls, comp)
+    ser = [[(x.kinetic_energy, x.enstrophy) for x in r.series] for r in runs]
+    assert ser[0] == ser[1] == ser[2]
+
+
+@pytest.mark.parametrize("preset", ["DP", "SPDP", "HPSP"])
+def test_weak_scaling_grid_replicates(b200, preset):
+    """z_periods = P stacked TGV periods on P slabs (the weak-scaling
+    configuration): every period is bitwise the single-cube run, and K is
+    the cube's K (same mean over P exact copies, within 1 ulp-scale sums)."""
+    n, P = 24, 3
+    one = b200_solver(b200, n, preset)
+    big = b200.Solver(b200.GridSpec(n, z_periods=P), b200.resolve_preset(preset), "storesome",
+                      b200.FlowParams(0.1, 1600.0, 0.72, 1.4, True), "Blaisdell",
+                      decomp=b200.Decomposition(pz=P))
+    one.init_tgv()
+    big.init_tgv()
+    r1 = one.advance(b200.StepConfig(0.002, 3, 3))
+    r2 = big.advance(b200.StepConfig(0.002, 3, 3))
+    for cls in (0, 1):
+        for comp in range(5):
+            a = one.get_field(cls, comp)
+            b = big.get_field(cls, comp)
+            assert b.shape == (n * P, n, n)
+            for k in range(P):
+                assert same_bits(a, b[k * n:(k + 1) * n]), (cls, comp, k)
+    for x, y in zip(r1.series, r2.series):
+        assert abs(x.kinetic_energy - y.kinetic_energy) <= 1e-14 * abs(x.kinetic_energy)
+        assert abs(x.enstrophy - y.enstrophy) <= 1e-13 * abs(x.enstrophy)
+    e = big.get_field_ext(0, 0)
+    assert e.shape == (n * P + 8, n + 8, n + 8)
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("preset", ["DP", "SPDP", "HPSP"])
 def test_64_cubed_step(b200, preset):
