@@ -38,7 +38,20 @@ __device__ __forceinline__ W2 RKV(int round, int kind, W2 v) {
     return round ? round_kind_v<W2>(kind, v) : v;
 }
 
+// constant slots of FusedArgs::kb, each pre-converted on the host to the
+// type it is used in (bits of the scalar, or of the two-lane broadcast for
+// types of <= 4 bytes), so the kernels read them as constant-bank operands
+enum KSlot {
+    K_R = 0, K_R2, K_INV_RE, K_THIRD, K_TWO_THIRDS, K_KAPPA, K_COEF0,  // residual compute type
+    K_R_STAGE = K_COEF0 + 7,                                           // wk compute type
+    K_HALF, K_GM1, K_GM2,                                              // wk compute type
+    K_A_C, K_DT_C,                                                     // rk compute type
+    K_B_C,                                                             // q compute type
+    K_NSLOTS
+};
+
 struct FusedArgs {
+    unsigned long long kb[K_NSLOTS];
     Geo g;
     const void* qin;
     void* qout;
@@ -123,28 +136,80 @@ __device__ __forceinline__ T ring_grad(const PT* const pl[5], int q, int i, int 
     return cvt<T>(round_kind<WC>(sc.kind[i == 3 ? 9 + j : i * 3 + j], v));
 }
 
+// operands of the stage update at one point, loaded ahead of their use
+// (the loads' latency overlaps the residual arithmetic)
+template <class QS, class TS>
+struct RkIn {
+    TS qt;
+    QS q;
+};
+template <class QS, class TS>
+__device__ __forceinline__ RkIn<QS, TS> rk_load(const FusedArgs& a, int comp, int c, long long o) {
+    const long long ir = ((long long)c * 5 + comp) * a.g.plane + o;
+    const long long iq = ((long long)(c + kHalo) * 5 + comp) * a.g.plane + o;
+    RkIn<QS, TS> v;
+    v.qt = a.kc.skip_a ? TS() : __ldg((const TS*)a.qtin + ir);
+    v.q = __ldg((const QS*)a.qin + iq);
+    return v;
+}
+
+// MPFD_RKC: when phase C loads its stage-update operands -- 0 after the
+// residual, 1 before it (registers live across the residual), 2 after it
+// with an L2 prefetch issued at the start of the iteration
+#ifndef MPFD_RKC
+#define MPFD_RKC 1
+#endif
+#ifndef MPFD_RAW_PF
+#define MPFD_RAW_PF 1
+#endif
+template <class QS, class TS>
+__device__ __forceinline__ void rk_prefetch_l2(const FusedArgs& a, int comp, int c, long long o) {
+    const long long ir = ((long long)c * 5 + comp) * a.g.plane + o;
+    const long long iq = ((long long)(c + kHalo) * 5 + comp) * a.g.plane + o;
+    if (!a.kc.skip_a) asm volatile("prefetch.global.L2 [%0];" ::"l"((const TS*)a.qtin + ir));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"((const QS*)a.qin + iq));
+}
+
 template <class QS, class TS, class RS, class TC, class QC>
-__device__ __forceinline__ void rk_point(const FusedArgs& a, int comp, int c, long long o, RS rs, int x, int y) {
+__device__ __forceinline__ void rk_point(const FusedArgs& a, int comp, int c, long long o, RS rs,
+                                         RkIn<QS, TS> in, int x, int y) {
     const Geo& g = a.g;
     const long long ir = ((long long)c * 5 + comp) * g.plane + o;
     const long long iq = ((long long)(c + kHalo) * 5 + comp) * g.plane + o;
-    const TC a_c = cvt<TC>(a.kc.a_c), dt_c = cvt<TC>(a.kc.dt_c);
-    const QC b_c = cvt<QC>(a.kc.b_c);
+    const TC a_c = kget<TC>(a.kb[K_A_C]), dt_c = kget<TC>(a.kb[K_DT_C]);
+    const QC b_c = kget<QC>(a.kb[K_B_C]);
     const TC t = Op<TC>::mul(dt_c, cvt<TC>(rs));
-    const TC v = a.kc.skip_a ? t : Op<TC>::add(Op<TC>::mul(a_c, cvt<TC>(((const TS*)a.qtin)[ir])), t);
+    const TC v = a.kc.skip_a ? t : Op<TC>::add(Op<TC>::mul(a_c, cvt<TC>(in.qt)), t);
     const TS vs = cvt<TS>(v);
     ((TS*)a.qtout)[ir] = vs;
-    const QC nq = Op<QC>::add(cvt<QC>(((const QS*)a.qin)[iq]), Op<QC>::mul(b_c, cvt<QC>(vs)));
+    const QC nq = Op<QC>::add(cvt<QC>(in.q), Op<QC>::mul(b_c, cvt<QC>(vs)));
     const QS ns = cvt<QS>(nq);
     ((QS*)a.qout)[iq] = ns;
     if (a.write_r) ((RS*)a.r)[ir] = rs;
-    const unsigned long long gi = ((unsigned long long)(g.z0 + c) * g.ny + y) * g.nx + x;
-    if (!isfinite(cvt<double>(rs))) record_div(a.div, 1, comp, gi, a.iter, a.sub);
-    if (!isfinite(cvt<double>(ns))) record_div(a.div, 2, comp, gi, a.iter, a.sub);
+    if (nonfinite(rs) | nonfinite(ns)) {
+        const unsigned long long gi = ((unsigned long long)(g.z0 + c) * g.ny + y) * g.nx + x;
+        if (nonfinite(rs)) record_div(a.div, 1, comp, gi, a.iter, a.sub);
+        if (nonfinite(ns)) record_div(a.div, 2, comp, gi, a.iter, a.sub);
+    }
 }
 
+// cp.async (LDGSTS) of one 4/8/16-byte element into shared memory
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(gmem), "n"(BYTES));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// STAGE: the next plane's Q (raw storage type, R4 box) is copied into shared
+// memory by cp.async while the current plane computes, instead of a
+// register prefetch
 template <class QS, class TS, class RS, class PT, class WC, class T, class TC, class QC, bool STAGED, class TL,
-          int MINB, unsigned SPL>
+          int MINB, unsigned SPL, bool STAGE>
 __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
     // a substep after a divergence is a no-op; launches of the substep that
     // diverged (interior and boundary of an overlapped substep) all run, so
@@ -169,9 +234,9 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
     const int p4 = (ty + 4) * TL::R4X + tx + 4;
     const int p2 = (ty + 2) * TL::R2X + tx + 2;
 
-    const RC<T> c(a.rc);
-    const WC rw = cvt<WC>(a.sc.r_stage);
-    const WC half = cvt<WC>(a.pc.half), gm1 = cvt<WC>(a.pc.gm1), gM2 = cvt<WC>(a.pc.gM2);
+    const RC<T> c(a.kb, a.rc);
+    const WC rw = kget<WC>(a.kb[K_R_STAGE]);
+    const WC half = kget<WC>(a.kb[K_HALF]), gm1 = kget<WC>(a.kb[K_GM1]), gM2 = kget<WC>(a.kb[K_GM2]);
     const QS* qin = (const QS*)a.qin;
 
     // register windows along z (own column): level-2 z-operands of planes
@@ -186,9 +251,16 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
     constexpr int KPF = (TL::R4N + TL::NT - 1) / TL::NT;
     // when primitives and residual compute in the same type, Q is narrowed
     // once on arrival (the only two uses both narrow to that type)
+    // raw storage values (MPFD_RAW_PF): a narrowing conversion here would
+    // wait on the load
+#if MPFD_RAW_PF
+    using PFT = QS;
+#else
     using PFT = typename std::conditional<std::is_same<WC, T>::value, T, QS>::type;
+#endif
     int rim_off[KPF];
-    PFT pf[KPF][5];
+    PFT pf[STAGE ? 1 : KPF][5];
+    QS* Sg = (QS*)(smem_raw + ((SM::total + 15) & ~(size_t)15));  // STAGE: [5][R4N] raw Q of the next plane
     const bool fastwrap = g.nx >= TL::TX + 8 && g.ny >= TL::TY + 8;
 #pragma unroll
     for (int k = 0; k < KPF; ++k) {
@@ -207,9 +279,27 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             if (yy < 0) yy += g.ny;
         }
         rim_off[k] = yy * g.nx + xx;
-        const QS* qp = qin + (long long)(zs - 4 + kHalo) * 5 * g.plane + rim_off[k];
+        if constexpr (!STAGE) {
+            const QS* qp = qin + (long long)(zs - 4 + kHalo) * 5 * g.plane + rim_off[k];
 #pragma unroll
-        for (int cc = 0; cc < 5; ++cc) pf[k][cc] = cvt<PFT>(qp[cc * g.plane]);
+            for (int cc = 0; cc < 5; ++cc) pf[k][cc] = cvt<PFT>(__ldg(qp + cc * g.plane));
+        }
+    }
+    auto stage_issue = [&](int p) {
+        const QS* qb = qin + (long long)(p + kHalo) * 5 * g.plane;
+#pragma unroll
+        for (int k = 0; k < KPF; ++k) {
+            const int i = tid + k * TL::NT;
+            if (i >= TL::R4N) break;
+#pragma unroll
+            for (int cc = 0; cc < 5; ++cc) cp_async<sizeof(QS)>(Sg + cc * TL::R4N + i, qb + cc * g.plane + rim_off[k]);
+        }
+        cp_async_commit();
+    };
+    if constexpr (STAGE) {
+        stage_issue(zs - 4);
+        cp_async_wait_all();
+        __syncthreads();
     }
 
     int slot = 0;  // ring slot of plane t
@@ -218,6 +308,19 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
     for (int i = 0; i < 5; ++i) sl[i] = i;
 
     for (int t = zs - 4; t < ze + 4; ++t) {
+        // stage-update operands of phase D (plane t-4, rhow and rhoE)
+        const bool do_d = t >= zs + 4 && own;
+        RkIn<QS, TS> ind[2];
+        if (do_d) {
+            ind[0] = rk_load<QS, TS>(a, 3, t - 4, o);
+            ind[1] = rk_load<QS, TS>(a, 4, t - 4, o);
+        }
+#if MPFD_RKC == 2
+        if (t >= zs + 2 && t < ze + 2 && own) {
+#pragma unroll
+            for (int comp = 0; comp < 3; ++comp) rk_prefetch_l2<QS, TS>(a, comp, t - 2, o);
+        }
+#endif
         // ---- A: primitives and Q of plane t on the rim ----------------------
         slot = sl[4];
 #pragma unroll
@@ -225,23 +328,28 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             const int i = tid + k * TL::NT;
             if (i >= TL::R4N) break;
             const int ry = i / TL::R4X, rx = i - ry * TL::R4X;
-            const PFT q0 = pf[k][0], q1 = pf[k][1], q2 = pf[k][2], q3 = pf[k][3], q4 = pf[k][4];
-            // prefetch plane t+1 for this point (consumed next iteration)
-            if (t + 1 < ze + 4) {
-                const QS* qp = qin + (long long)(t + 1 + kHalo) * 5 * g.plane + rim_off[k];
+            PFT q0, q1, q2, q3, q4;
+            if constexpr (STAGE) {
+                const QS* sp = Sg + i;
+                q0 = cvt<PFT>(sp[0]);
+                q1 = cvt<PFT>(sp[TL::R4N]);
+                q2 = cvt<PFT>(sp[2 * TL::R4N]);
+                q3 = cvt<PFT>(sp[3 * TL::R4N]);
+                q4 = cvt<PFT>(sp[4 * TL::R4N]);
+            } else {
+                const int kk = STAGE ? 0 : k;
+                q0 = pf[kk][0], q1 = pf[kk][1], q2 = pf[kk][2], q3 = pf[kk][3], q4 = pf[kk][4];
+                // prefetch plane t+1 for this point (consumed next iteration)
+                if (t + 1 < ze + 4) {
+                    const QS* qp = qin + (long long)(t + 1 + kHalo) * 5 * g.plane + rim_off[k];
 #pragma unroll
-                for (int cc = 0; cc < 5; ++cc) pf[k][cc] = cvt<PFT>(qp[cc * g.plane]);
+                    for (int cc = 0; cc < 5; ++cc) pf[kk][cc] = cvt<PFT>(__ldg(qp + cc * g.plane));
+                }
             }
             using O = Op<WC>;
             const WC rho = cvt<WC>(q0);
-            const WC ux = O::div(cvt<WC>(q1), rho);
-            const WC uy = O::div(cvt<WC>(q2), rho);
-            const WC uz = O::div(cvt<WC>(q3), rho);
-            const WC Et = O::div(cvt<WC>(q4), rho);
-            const WC kin = O::mul(half, O::add(O::add(O::mul(ux, ux), O::mul(uy, uy)), O::mul(uz, uz)));
-            const WC e = O::sub(Et, kin);
-            const WC pr = O::mul(gm1, O::mul(rho, e));
-            const WC Tv = O::div(O::mul(gM2, pr), rho);
+            const PrimOut<WC> pv = PrimCalc<WC>::run(rho, cvt<WC>(q1), cvt<WC>(q2), cvt<WC>(q3), cvt<WC>(q4), half, gm1, gM2);
+            const WC ux = pv.ux, uy = pv.uy, uz = pv.uz, pr = pv.pr, Tv = pv.Tv;
             PT* pp = Pr + slot * TL::R4N + i;
             constexpr int FS = TL::NRING * TL::R4N;
             pp[0] = cvt<PT>(RK1<WC>(a.pc.round, a.pc.kind[0], ux));
@@ -262,8 +370,7 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             // CTA, planes it owns, exactly once
             if (t >= zs && t < ze && rx >= 4 && rx < TL::TX + 4 && ry >= 4 && ry < TL::TY + 4 &&
                 x0 - 4 + rx < g.nx && y0 - 4 + ry < g.ny) {
-                const float rf = (float)cvt<double>(rho);
-                if (!(rf > 0.0f) || !isfinite(rf)) {
+                if (!Op<WC>::positive(rho) || nonfinite(rho)) {
                     const unsigned long long gi =
                         ((unsigned long long)(g.z0 + t) * g.ny + (y0 - 4 + ry)) * g.nx + (x0 - 4 + rx);
                     record_div(a.div, 0, 0, gi, a.iter, a.sub);
@@ -271,6 +378,9 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             }
         }
         __syncthreads();
+        if constexpr (STAGE) {
+            if (t + 1 < ze + 4) stage_issue(t + 1);
+        }
 
         const PT* plp[5];
 #pragma unroll
@@ -354,7 +464,7 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
 
         // ---- D: late residual of plane t-4 -> RK of rhow, rhoE ---------------
         // (runs before C so its deferred slot can be reused for plane t-2)
-        if (t >= zs + 4 && own) {
+        if (do_d) {
             T cw = Op<T>::zero(), tz = Op<T>::zero(), hz = Op<T>::zero();
             if (c.viscous) {
                 cw = d1v<T>(wdiv[0], wdiv[1], wdiv[3], wdiv[4], c.r);
@@ -364,8 +474,8 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             T rw_, rE;
             residual_late<T>(c, dfr[0], cw, tz, hz, rw_, rE);
             const int cpl = t - 4;
-            rk_point<QS, TS, RS, TC, QC>(a, 3, cpl, o, cvt<RS>(rw_), x, y);
-            rk_point<QS, TS, RS, TC, QC>(a, 4, cpl, o, cvt<RS>(rE), x, y);
+            rk_point<QS, TS, RS, TC, QC>(a, 3, cpl, o, cvt<RS>(rw_), ind[0], x, y);
+            rk_point<QS, TS, RS, TC, QC>(a, 4, cpl, o, cvt<RS>(rE), ind[1], x, y);
         }
         // deferred window: dfr[0] plane t-3, dfr[1] plane t-2 after this step
         if (t >= zs + 2) dfr[0] = dfr[1];
@@ -380,13 +490,23 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
                 acc.qp[i] = Qr + sl[i] * TL::R2N + p2;
             }
             acc.lp = Lb + p2;
+            const int cpl = t - 2;
+            RkIn<QS, TS> inc[3];
+#if MPFD_RKC == 1
+#pragma unroll
+            for (int comp = 0; comp < 3; ++comp) inc[comp] = rk_load<QS, TS>(a, comp, cpl, o);
+#endif
             T out[3];
             residual_early_dirwise<T, SPL>(c, acc, out, dfr[1]);
-            const int cpl = t - 2;
+#if MPFD_RKC != 1
+#pragma unroll
+            for (int comp = 0; comp < 3; ++comp) inc[comp] = rk_load<QS, TS>(a, comp, cpl, o);
+#endif
 #pragma unroll
             for (int comp = 0; comp < 3; ++comp)
-                rk_point<QS, TS, RS, TC, QC>(a, comp, cpl, o, cvt<RS>(out[comp]), x, y);
+                rk_point<QS, TS, RS, TC, QC>(a, comp, cpl, o, cvt<RS>(out[comp]), inc[comp], x, y);
         }
+        if constexpr (STAGE) cp_async_wait_all();
         __syncthreads();
         // rotate the ring: planes t-3..t+1
         const int s0 = sl[0];
@@ -398,10 +518,21 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
 
 // tile choice per compute type: DP keeps one 256-thread CTA per SM (the
 // rings need ~223 KB of shared memory); fp32 and fp16 fit two / three
-template <class T, class PT>
+// MPFD_STAGE1: one 512-thread CTA per SM on a 32 x 16 tile with cp.async
+// staging wherever the rings and the staging buffer fit (fp32 compute);
+// otherwise 256-thread CTAs on 32 x 8 with a register prefetch
+#ifndef MPFD_STAGE1
+#define MPFD_STAGE1 1
+#endif
+template <class T, class PT, class QS>
 struct FusedTile {
-    using TL = Tile<32, 8>;
-    static constexpr int MINB = sizeof(T) >= 8 || sizeof(PT) >= 8 ? 1 : 2;
+    using TLS = Tile<32, 16>;
+    static constexpr size_t SMEM_S =
+        ((FusedSmem<TLS, T, PT>::total + 15) & ~(size_t)15) + (size_t)5 * TLS::R4N * sizeof(QS);
+    static constexpr bool STAGE = MPFD_STAGE1 != 0 && sizeof(QS) >= 4 && SMEM_S <= 232448;
+    using TL = typename std::conditional<STAGE, TLS, Tile<32, 8>>::type;
+    static constexpr int MINB = STAGE ? 1 : (sizeof(T) >= 8 || sizeof(PT) >= 8 ? 1 : 2);
+    static constexpr size_t SMEM = STAGE ? SMEM_S : FusedSmem<TL, T, PT>::total;
 };
 
 }  // namespace mpfd_b200

@@ -81,9 +81,26 @@ __device__ __forceinline__ T2 ring_grad2(const PT* const pl[5], int q, int f, in
     return cvt<T2>(round_kind_v<WC2>(sc.kind[f == 3 ? 9 + j : f * 3 + j], v));
 }
 
+template <class QS, class TS>
+struct RkIn2 {
+    typename V2<TS>::type qt;
+    typename V2<QS>::type q;
+};
+template <class QS, class TS>
+__device__ __forceinline__ RkIn2<QS, TS> rk_load2(const FusedArgs& a, int comp, int c, long long o) {
+    using TS2 = typename V2<TS>::type;
+    using QS2 = typename V2<QS>::type;
+    const long long ir = ((long long)c * 5 + comp) * a.g.plane + o;
+    const long long iq = ((long long)(c + kHalo) * 5 + comp) * a.g.plane + o;
+    RkIn2<QS, TS> v;
+    v.qt = a.kc.skip_a ? TS2() : __ldg(reinterpret_cast<const TS2*>((const TS*)a.qtin + ir));
+    v.q = __ldg(reinterpret_cast<const QS2*>((const QS*)a.qin + iq));
+    return v;
+}
+
 template <class QS, class TS, class RS, class TC, class QC>
 __device__ __forceinline__ void rk_pair(const FusedArgs& a, int comp, int c, long long o,
-                                        typename V2<RS>::type rs, int x, int y) {
+                                        typename V2<RS>::type rs, RkIn2<QS, TS> in, int x, int y) {
     using TC2 = typename V2<TC>::type;
     using QC2 = typename V2<QC>::type;
     using TS2 = typename V2<TS>::type;
@@ -91,26 +108,30 @@ __device__ __forceinline__ void rk_pair(const FusedArgs& a, int comp, int c, lon
     const Geo& g = a.g;
     const long long ir = ((long long)c * 5 + comp) * g.plane + o;
     const long long iq = ((long long)(c + kHalo) * 5 + comp) * g.plane + o;
-    const TC2 a_c = cvt<TC2>(a.kc.a_c), dt_c = cvt<TC2>(a.kc.dt_c);
-    const QC2 b_c = cvt<QC2>(a.kc.b_c);
+    const TC2 a_c = kget<TC2>(a.kb[K_A_C]), dt_c = kget<TC2>(a.kb[K_DT_C]);
+    const QC2 b_c = kget<QC2>(a.kb[K_B_C]);
     const TC2 t = Op<TC2>::mul(dt_c, cvt<TC2>(rs));
-    const TC2 v = a.kc.skip_a ? t : Op<TC2>::add(Op<TC2>::mul(a_c, cvt<TC2>(ldv<TS>((const TS*)a.qtin + ir))), t);
+    const TC2 v = a.kc.skip_a ? t : Op<TC2>::add(Op<TC2>::mul(a_c, cvt<TC2>(in.qt)), t);
     const TS2 vs = cvt<TS2>(v);
     stv<TS>((TS*)a.qtout + ir, vs);
-    const QC2 nq = Op<QC2>::add(cvt<QC2>(ldv<QS>((const QS*)a.qin + iq)), Op<QC2>::mul(b_c, cvt<QC2>(vs)));
+    const QC2 nq = Op<QC2>::add(cvt<QC2>(in.q), Op<QC2>::mul(b_c, cvt<QC2>(vs)));
     const QS2 ns = cvt<QS2>(nq);
     stv<QS>((QS*)a.qout + iq, ns);
     if (a.write_r) stv<RS>((RS*)a.r + ir, rs);
-    const unsigned long long gi = ((unsigned long long)(g.z0 + c) * g.ny + y) * g.nx + x;
-    if (!isfinite(cvt<double>(lo(rs)))) record_div(a.div, 1, comp, gi, a.iter, a.sub);
-    if (!isfinite(cvt<double>(hi(rs)))) record_div(a.div, 1, comp, gi + 1, a.iter, a.sub);
-    if (!isfinite(cvt<double>(lo(ns)))) record_div(a.div, 2, comp, gi, a.iter, a.sub);
-    if (!isfinite(cvt<double>(hi(ns)))) record_div(a.div, 2, comp, gi + 1, a.iter, a.sub);
+    if (nonfinite2(rs) | nonfinite2(ns)) {
+        const unsigned long long gi = ((unsigned long long)(g.z0 + c) * g.ny + y) * g.nx + x;
+        if (nonfinite(lo(rs))) record_div(a.div, 1, comp, gi, a.iter, a.sub);
+        if (nonfinite(hi(rs))) record_div(a.div, 1, comp, gi + 1, a.iter, a.sub);
+        if (nonfinite(lo(ns))) record_div(a.div, 2, comp, gi, a.iter, a.sub);
+        if (nonfinite(hi(ns))) record_div(a.div, 2, comp, gi + 1, a.iter, a.sub);
+    }
 }
 
-// TL: tile in POINTS (TX = 2 * threads along x)
+// TL: tile in POINTS (TX = 2 * threads along x).  STAGE: the next plane's Q
+// (raw storage type, R4 box) is copied into shared memory by cp.async while
+// the current plane computes, instead of a register prefetch.
 template <class QS, class TS, class RS, class PT, class WC, class T, class TC, class QC, bool STAGED, class TL,
-          int MINB, unsigned SPL>
+          int MINB, unsigned SPL, bool STAGE>
 __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
     // a substep after a divergence is a no-op; launches of the substep that
     // diverged (interior and boundary of an overlapped substep) all run, so
@@ -143,9 +164,9 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
     const int p4 = (ty + 4) * TL::R4X + 2 * tx + 4;
     const int p2 = (ty + 2) * TL::R2X + 2 * tx + 2;
 
-    const RC<T2> c(a.rc);
-    const WC2 rw = cvt<WC2>(a.sc.r_stage);
-    const WC2 half = cvt<WC2>(a.pc.half), gm1 = cvt<WC2>(a.pc.gm1), gM2 = cvt<WC2>(a.pc.gM2);
+    const RC<T2> c(a.kb, a.rc);
+    const WC2 rw = kget<WC2>(a.kb[K_R_STAGE]);
+    const WC2 half = kget<WC2>(a.kb[K_HALF]), gm1 = kget<WC2>(a.kb[K_GM1]), gM2 = kget<WC2>(a.kb[K_GM2]);
     const QS* qin = (const QS*)a.qin;
 
     T2 wdiv[5], wgz[5], wdt[5];
@@ -154,10 +175,18 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
     for (int i = 0; i < 5; ++i) wdiv[i] = wgz[i] = wdt[i] = Op<T2>::zero();
 
     constexpr int KPF = (R4NP + NT - 1) / NT;
+    // raw storage values (MPFD_RAW_PF): a narrowing conversion here would
+    // wait on the load
+#if MPFD_RAW_PF
+    using PFS = QS;
+#else
     using PFS = typename std::conditional<std::is_same<WC, T>::value, T, QS>::type;
+#endif
     using PF2 = typename V2<PFS>::type;
     int rim_off[KPF];
-    PF2 pf[KPF][5];
+    PF2 pf[STAGE ? 1 : KPF][5];
+    using QS2 = typename V2<QS>::type;
+    QS* Sg = (QS*)(smem_raw + ((SM::total + 15) & ~(size_t)15));  // STAGE: [5][R4N] raw Q of the next plane
     const bool fastwrap = g.nx >= TL::TX + 8 && g.ny >= TL::TY + 8;
 #pragma unroll
     for (int k = 0; k < KPF; ++k) {
@@ -176,9 +205,29 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
             if (yy < 0) yy += g.ny;
         }
         rim_off[k] = yy * g.nx + xx;
-        const QS* qp = qin + (long long)(zs - 4 + kHalo) * 5 * g.plane + rim_off[k];
+        if constexpr (!STAGE) {
+            const QS* qp = qin + (long long)(zs - 4 + kHalo) * 5 * g.plane + rim_off[k];
 #pragma unroll
-        for (int cc = 0; cc < 5; ++cc) pf[k][cc] = cvt<PF2>(ldv<QS>(qp + cc * g.plane));
+            for (int cc = 0; cc < 5; ++cc) pf[k][cc] = cvt<PF2>(__ldg(reinterpret_cast<const QS2*>(qp + cc * g.plane)));
+        }
+    }
+    // STAGE: copy plane p's Q on this thread's rim pairs into Sg
+    auto stage_issue = [&](int p) {
+        const QS* qb = qin + (long long)(p + kHalo) * 5 * g.plane;
+#pragma unroll
+        for (int k = 0; k < KPF; ++k) {
+            const int i = tid + k * NT;
+            if (i >= R4NP) break;
+#pragma unroll
+            for (int cc = 0; cc < 5; ++cc)
+                cp_async<2 * sizeof(QS)>(Sg + cc * TL::R4N + 2 * i, qb + cc * g.plane + rim_off[k]);
+        }
+        cp_async_commit();
+    };
+    if constexpr (STAGE) {
+        stage_issue(zs - 4);
+        cp_async_wait_all();
+        __syncthreads();
     }
 
     int sl[5];
@@ -186,6 +235,19 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
     for (int i = 0; i < 5; ++i) sl[i] = i;
 
     for (int t = zs - 4; t < ze + 4; ++t) {
+        // stage-update operands of phase D (plane t-4, rhow and rhoE)
+        const bool do_d = t >= zs + 4 && own;
+        RkIn2<QS, TS> ind[2];
+        if (do_d) {
+            ind[0] = rk_load2<QS, TS>(a, 3, t - 4, o);
+            ind[1] = rk_load2<QS, TS>(a, 4, t - 4, o);
+        }
+#if MPFD_RKC == 2
+        if (t >= zs + 2 && t < ze + 2 && own) {
+#pragma unroll
+            for (int comp = 0; comp < 3; ++comp) rk_prefetch_l2<QS, TS>(a, comp, t - 2, o);
+        }
+#endif
         // ---- A: primitives and Q of plane t ------------------------------------
         const int slot = sl[4];
 #pragma unroll
@@ -193,22 +255,27 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
             const int i = tid + k * NT;
             if (i >= R4NP) break;
             const int ry = i / R4P, rx = 2 * (i - ry * R4P);
-            const PF2 q0 = pf[k][0], q1 = pf[k][1], q2 = pf[k][2], q3 = pf[k][3], q4 = pf[k][4];
-            if (t + 1 < ze + 4) {
-                const QS* qp = qin + (long long)(t + 1 + kHalo) * 5 * g.plane + rim_off[k];
+            PF2 q0, q1, q2, q3, q4;
+            if constexpr (STAGE) {
+                const QS* sp = Sg + 2 * i;
+                q0 = cvt<PF2>(ldv<QS>(sp));
+                q1 = cvt<PF2>(ldv<QS>(sp + TL::R4N));
+                q2 = cvt<PF2>(ldv<QS>(sp + 2 * TL::R4N));
+                q3 = cvt<PF2>(ldv<QS>(sp + 3 * TL::R4N));
+                q4 = cvt<PF2>(ldv<QS>(sp + 4 * TL::R4N));
+            } else {
+                const int kk = STAGE ? 0 : k;
+                q0 = pf[kk][0], q1 = pf[kk][1], q2 = pf[kk][2], q3 = pf[kk][3], q4 = pf[kk][4];
+                if (t + 1 < ze + 4) {
+                    const QS* qp = qin + (long long)(t + 1 + kHalo) * 5 * g.plane + rim_off[k];
 #pragma unroll
-                for (int cc = 0; cc < 5; ++cc) pf[k][cc] = cvt<PF2>(ldv<QS>(qp + cc * g.plane));
+                    for (int cc = 0; cc < 5; ++cc) pf[kk][cc] = cvt<PF2>(__ldg(reinterpret_cast<const QS2*>(qp + cc * g.plane)));
+                }
             }
             using O = Op<WC2>;
             const WC2 rho = cvt<WC2>(q0);
-            const WC2 ux = O::div(cvt<WC2>(q1), rho);
-            const WC2 uy = O::div(cvt<WC2>(q2), rho);
-            const WC2 uz = O::div(cvt<WC2>(q3), rho);
-            const WC2 Et = O::div(cvt<WC2>(q4), rho);
-            const WC2 kin = O::mul(half, O::add(O::add(O::mul(ux, ux), O::mul(uy, uy)), O::mul(uz, uz)));
-            const WC2 e = O::sub(Et, kin);
-            const WC2 pr = O::mul(gm1, O::mul(rho, e));
-            const WC2 Tv = O::div(O::mul(gM2, pr), rho);
+            const PrimOut<WC2> pv = PrimCalc<WC2>::run(rho, cvt<WC2>(q1), cvt<WC2>(q2), cvt<WC2>(q3), cvt<WC2>(q4), half, gm1, gM2);
+            const WC2 ux = pv.ux, uy = pv.uy, uz = pv.uz, pr = pv.pr, Tv = pv.Tv;
             constexpr int FS = TL::NRING * TL::R4N;
             PT* pp = Pr + slot * TL::R4N + ry * TL::R4X + rx;
             stv<PT>(pp, cvt<PT2>(RKV<WC2>(a.pc.round, a.pc.kind[0], ux)));
@@ -228,14 +295,21 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
             }
             if (t >= zs && t < ze && rx >= 4 && rx < TL::TX + 4 && ry >= 4 && ry < TL::TY + 4 &&
                 x0 - 4 + rx < g.nx && y0 - 4 + ry < g.ny) {
-                const float r0 = (float)cvt<double>(lo(rho)), r1 = (float)cvt<double>(hi(rho));
-                const unsigned long long gi =
-                    ((unsigned long long)(g.z0 + t) * g.ny + (y0 - 4 + ry)) * g.nx + (x0 - 4 + rx);
-                if (!(r0 > 0.0f) || !isfinite(r0)) record_div(a.div, 0, 0, gi, a.iter, a.sub);
-                if (!(r1 > 0.0f) || !isfinite(r1)) record_div(a.div, 0, 0, gi + 1, a.iter, a.sub);
+                using OS = Op<WC>;
+                const bool b0 = !OS::positive(lo(rho)) || nonfinite(lo(rho));
+                const bool b1 = !OS::positive(hi(rho)) || nonfinite(hi(rho));
+                if (b0 | b1) {
+                    const unsigned long long gi =
+                        ((unsigned long long)(g.z0 + t) * g.ny + (y0 - 4 + ry)) * g.nx + (x0 - 4 + rx);
+                    if (b0) record_div(a.div, 0, 0, gi, a.iter, a.sub);
+                    if (b1) record_div(a.div, 0, 0, gi + 1, a.iter, a.sub);
+                }
             }
         }
         __syncthreads();
+        if constexpr (STAGE) {
+            if (t + 1 < ze + 4) stage_issue(t + 1);
+        }
 
         const PT* plp[5];
 #pragma unroll
@@ -318,7 +392,7 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
         __syncthreads();
 
         // ---- D: late residual of plane t-4 -> RK of rhow, rhoE -------------
-        if (t >= zs + 4 && own) {
+        if (do_d) {
             T2 cw = Op<T2>::zero(), tz = Op<T2>::zero(), hz = Op<T2>::zero();
             if (c.viscous) {
                 cw = d1v<T2>(wdiv[0], wdiv[1], wdiv[3], wdiv[4], c.r);
@@ -327,8 +401,8 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
             }
             T2 rw_, rE;
             residual_late<T2>(c, dfr[0], cw, tz, hz, rw_, rE);
-            rk_pair<QS, TS, RS, TC, QC>(a, 3, t - 4, o, cvt<RS2>(rw_), x, y);
-            rk_pair<QS, TS, RS, TC, QC>(a, 4, t - 4, o, cvt<RS2>(rE), x, y);
+            rk_pair<QS, TS, RS, TC, QC>(a, 3, t - 4, o, cvt<RS2>(rw_), ind[0], x, y);
+            rk_pair<QS, TS, RS, TC, QC>(a, 4, t - 4, o, cvt<RS2>(rE), ind[1], x, y);
         }
         if (t >= zs + 2) dfr[0] = dfr[1];
 
@@ -342,12 +416,22 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
                 acc.qp[i] = Qr + sl[i] * TL::R2N + p2;
             }
             acc.lp = Lb + p2;
+            RkIn2<QS, TS> inc[3];
+#if MPFD_RKC == 1
+#pragma unroll
+            for (int comp = 0; comp < 3; ++comp) inc[comp] = rk_load2<QS, TS>(a, comp, t - 2, o);
+#endif
             T2 out[3];
             residual_early_dirwise<T2, SPL>(c, acc, out, dfr[1]);
+#if MPFD_RKC != 1
+#pragma unroll
+            for (int comp = 0; comp < 3; ++comp) inc[comp] = rk_load2<QS, TS>(a, comp, t - 2, o);
+#endif
 #pragma unroll
             for (int comp = 0; comp < 3; ++comp)
-                rk_pair<QS, TS, RS, TC, QC>(a, comp, t - 2, o, cvt<RS2>(out[comp]), x, y);
+                rk_pair<QS, TS, RS, TC, QC>(a, comp, t - 2, o, cvt<RS2>(out[comp]), inc[comp], x, y);
         }
+        if constexpr (STAGE) cp_async_wait_all();
         __syncthreads();
         const int s0 = sl[0];
 #pragma unroll
@@ -385,15 +469,27 @@ struct FusedPlan {
     // storage (StoreRound; per-name overrides wider than the class are
     // rejected for the fused path by the host)
     using PT = typename KT<WK>::type;
-    using FT = FusedTile<T, PT>;
+    using FT = FusedTile<T, PT, QS>;
     using TL = typename FT::TL;
 
     // two-point kernel: fp16 / fp32 compute (all of WC, T, PT <= 4 bytes)
     // (packed fp32 measured slower than scalar fp32 at 2 CTAs/SM: the
     // contraction barrier costs an ALU op per multiply; fp16 pairs are native)
     static constexpr bool PAIR = sizeof(T) == 2 && sizeof(WC) <= 4 && sizeof(PT) <= 4;
-    using TL2 = Tile<64, 8>;
-    static constexpr int MINB2 = (sizeof(T) == 2 && sizeof(PT) == 2) ? 2 : 1;
+#ifndef MPFD_STAGE2
+#define MPFD_STAGE2 1
+#endif
+    // STAGE2: one 512-thread CTA per SM on a 64 x 16 tile with the next
+    // plane's Q staged by cp.async; otherwise two 256-thread CTAs on 64 x 8
+    // with a register prefetch
+    static constexpr size_t SMEM2S =
+        ((FusedSmem<Tile<64, 16>, T, PT>::total + 15) & ~(size_t)15) + (size_t)5 * Tile<64, 16>::R4N * sizeof(QS);
+    static constexpr bool STAGE2 = MPFD_STAGE2 != 0 && SMEM2S <= 232448;
+    using TL2 = typename std::conditional<STAGE2, Tile<64, 16>, Tile<64, 8>>::type;
+    static constexpr int MINB2 = STAGE2 ? 1 : ((sizeof(T) == 2 && sizeof(PT) == 2) ? 2 : 1);
+    static constexpr size_t SMEM2 =
+        STAGE2 ? ((FusedSmem<TL2, T, PT>::total + 15) & ~(size_t)15) + (size_t)5 * TL2::R4N * sizeof(QS)
+               : FusedSmem<TL2, T, PT>::total;
 
     static int z_range(const Geo& g, int nz, int tx, int ty, int minb) {
         // z planes per CTA: about 8 waves of CTAs over the 148 SMs, but at
@@ -408,8 +504,8 @@ struct FusedPlan {
     static void go(FusedArgs a, cudaStream_t st) {
         if constexpr (PAIR) {
             if (a.g.nx % 2 == 0) {
-            auto kern = k_fused2<QS, TS, RS, PT, WC, T, TC, QC, ST, TL2, MINB2, SPL>;
-            constexpr size_t smem = FusedSmem<TL2, T, PT>::total;
+            auto kern = k_fused2<QS, TS, RS, PT, WC, T, TC, QC, ST, TL2, MINB2, SPL, STAGE2>;
+            constexpr size_t smem = SMEM2;
             static bool attr = false;
             if (!attr) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -422,8 +518,8 @@ struct FusedPlan {
             return;
             }
         }
-        auto kern = k_fused<QS, TS, RS, PT, WC, T, TC, QC, ST, TL, FT::MINB, SPL>;
-        constexpr size_t smem = FusedSmem<TL, T, PT>::total;
+        auto kern = k_fused<QS, TS, RS, PT, WC, T, TC, QC, ST, TL, FT::MINB, SPL, FT::STAGE>;
+        constexpr size_t smem = FT::SMEM;
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -439,6 +535,21 @@ struct FusedPlan {
                        void* r, const PrimConsts& pc, const ResConsts& rc, const StageConsts& sc, bool staged,
                        const RkConsts& kc, bool write_r, DevDiv* div, int iter, int sub, int zlo, int zhi) {
         FusedArgs a;
+        using KT_ = KBits<T>;
+        a.kb[K_R] = KT_::of(rc.r);
+        a.kb[K_R2] = KT_::of(rc.r2);
+        a.kb[K_INV_RE] = KT_::of(rc.inv_re);
+        a.kb[K_THIRD] = KT_::of(rc.third);
+        a.kb[K_TWO_THIRDS] = KT_::of(rc.two_thirds);
+        a.kb[K_KAPPA] = KT_::of(rc.kappa);
+        for (int i = 0; i < 7; ++i) a.kb[K_COEF0 + i] = KT_::of(rc.coef[i]);
+        a.kb[K_R_STAGE] = KBits<WC>::of(sc.r_stage);
+        a.kb[K_HALF] = KBits<WC>::of(pc.half);
+        a.kb[K_GM1] = KBits<WC>::of(pc.gm1);
+        a.kb[K_GM2] = KBits<WC>::of(pc.gM2);
+        a.kb[K_A_C] = KBits<TC>::of(kc.a_c);
+        a.kb[K_DT_C] = KBits<TC>::of(kc.dt_c);
+        a.kb[K_B_C] = KBits<QC>::of(kc.b_c);
         a.g = g;
         a.zlo = zlo;
         a.zhi = zhi;

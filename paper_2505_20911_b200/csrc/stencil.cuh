@@ -46,6 +46,19 @@ struct RC {
         nz = c.nz;
         viscous = c.viscous;
     }
+    // from constant slots pre-converted on the host (kernels_fused.cuh KSlot)
+    __device__ __forceinline__ RC(const unsigned long long* kb, const ResConsts& c) {
+        r = kget<T>(kb[0]);
+        r2 = kget<T>(kb[1]);
+        inv_re = kget<T>(kb[2]);
+        third = kget<T>(kb[3]);
+        two_thirds = kget<T>(kb[4]);
+        kappa = kget<T>(kb[5]);
+#pragma unroll
+        for (int i = 0; i < 7; ++i) coef[i] = kget<T>(kb[6 + i]);
+        nz = c.nz;
+        viscous = c.viscous;
+    }
 };
 
 // d1 (kernels.hpp:139-144 / physics.cpp:71-80):

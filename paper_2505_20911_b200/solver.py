@@ -26,7 +26,8 @@ from typing import Dict, List, Optional, Tuple
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-library_path = os.path.join(HERE, "libmpfd_b200.so")
+# MPFD_B200_LIB selects an alternative in-tree build (developer A/B runs)
+library_path = os.environ.get("MPFD_B200_LIB") or os.path.join(HERE, "libmpfd_b200.so")
 
 B16, B32, B64 = 0, 1, 2
 STRICT, STOREROUND = 0, 1
