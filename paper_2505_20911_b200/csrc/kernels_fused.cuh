@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
     const int p4 = (ty + 4) * TL::R4X + tx + 4;
     const int p2 = (ty + 2) * TL::R2X + tx + 2;
 
-    const RC<T> c(a.kb, a.rc);
+    RC<T> c(a.kb, a.rc);
+    if constexpr (SPL != 0) c.viscous = 1;  // the fixed-split instance is launched for viscous runs only
     const WC rw = kget<WC>(a.kb[K_R_STAGE]);
     const WC half = kget<WC>(a.kb[K_HALF]), gm1 = kget<WC>(a.kb[K_GM1]), gM2 = kget<WC>(a.kb[K_GM2]);
     const QS* qin = (const QS*)a.qin;
@@ -339,12 +340,6 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             } else {
                 const int kk = STAGE ? 0 : k;
                 q0 = pf[kk][0], q1 = pf[kk][1], q2 = pf[kk][2], q3 = pf[kk][3], q4 = pf[kk][4];
-                // prefetch plane t+1 for this point (consumed next iteration)
-                if (t + 1 < ze + 4) {
-                    const QS* qp = qin + (long long)(t + 1 + kHalo) * 5 * g.plane + rim_off[k];
-#pragma unroll
-                    for (int cc = 0; cc < 5; ++cc) pf[kk][cc] = cvt<PFT>(__ldg(qp + cc * g.plane));
-                }
             }
             using O = Op<WC>;
             const WC rho = cvt<WC>(q0);
@@ -374,6 +369,15 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
                     const unsigned long long gi =
                         ((unsigned long long)(g.z0 + t) * g.ny + (y0 - 4 + ry)) * g.nx + (x0 - 4 + rx);
                     record_div(a.div, 0, 0, gi, a.iter, a.sub);
+                }
+            }
+            // register prefetch of plane t+1 for this point, issued after its
+            // values were consumed (reuses their registers, no copies)
+            if constexpr (!STAGE) {
+                if (t + 1 < ze + 4) {
+                    const QS* qp = qin + (long long)(t + 1 + kHalo) * 5 * g.plane + rim_off[k];
+#pragma unroll
+                    for (int cc = 0; cc < 5; ++cc) pf[k][cc] = cvt<PFT>(__ldg(qp + cc * g.plane));
                 }
             }
         }
@@ -478,7 +482,7 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             rk_point<QS, TS, RS, TC, QC>(a, 4, cpl, o, cvt<RS>(rE), ind[1], x, y);
         }
         // deferred window: dfr[0] plane t-3, dfr[1] plane t-2 after this step
-        if (t >= zs + 2) dfr[0] = dfr[1];
+        dfr[0] = dfr[1];  // (unused until phase D first runs at t = zs + 4)
 
         // ---- C: early residual of plane t-2 -> RK of rho, rhou, rhov --------
         if (t >= zs + 2 && t < ze + 2 && own) {

@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
     const int p4 = (ty + 4) * TL::R4X + 2 * tx + 4;
     const int p2 = (ty + 2) * TL::R2X + 2 * tx + 2;
 
-    const RC<T2> c(a.kb, a.rc);
+    RC<T2> c(a.kb, a.rc);
+    if constexpr (SPL != 0) c.viscous = 1;  // the fixed-split instance is launched for viscous runs only
     const WC2 rw = kget<WC2>(a.kb[K_R_STAGE]);
     const WC2 half = kget<WC2>(a.kb[K_HALF]), gm1 = kget<WC2>(a.kb[K_GM1]), gM2 = kget<WC2>(a.kb[K_GM2]);
     const QS* qin = (const QS*)a.qin;
@@ -266,11 +267,6 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
             } else {
                 const int kk = STAGE ? 0 : k;
                 q0 = pf[kk][0], q1 = pf[kk][1], q2 = pf[kk][2], q3 = pf[kk][3], q4 = pf[kk][4];
-                if (t + 1 < ze + 4) {
-                    const QS* qp = qin + (long long)(t + 1 + kHalo) * 5 * g.plane + rim_off[k];
-#pragma unroll
-                    for (int cc = 0; cc < 5; ++cc) pf[kk][cc] = cvt<PF2>(__ldg(reinterpret_cast<const QS2*>(qp + cc * g.plane)));
-                }
             }
             using O = Op<WC2>;
             const WC2 rho = cvt<WC2>(q0);
@@ -303,6 +299,13 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
                         ((unsigned long long)(g.z0 + t) * g.ny + (y0 - 4 + ry)) * g.nx + (x0 - 4 + rx);
                     if (b0) record_div(a.div, 0, 0, gi, a.iter, a.sub);
                     if (b1) record_div(a.div, 0, 0, gi + 1, a.iter, a.sub);
+                }
+            }
+            if constexpr (!STAGE) {
+                if (t + 1 < ze + 4) {
+                    const QS* qp = qin + (long long)(t + 1 + kHalo) * 5 * g.plane + rim_off[k];
+#pragma unroll
+                    for (int cc = 0; cc < 5; ++cc) pf[k][cc] = cvt<PF2>(__ldg(reinterpret_cast<const QS2*>(qp + cc * g.plane)));
                 }
             }
         }
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
             rk_pair<QS, TS, RS, TC, QC>(a, 3, t - 4, o, cvt<RS2>(rw_), ind[0], x, y);
             rk_pair<QS, TS, RS, TC, QC>(a, 4, t - 4, o, cvt<RS2>(rE), ind[1], x, y);
         }
-        if (t >= zs + 2) dfr[0] = dfr[1];
+        dfr[0] = dfr[1];  // (unused until phase D first runs at t = zs + 4)
 
         // ---- C: early residual of plane t-2 -> RK of rho, rhou, rhov -------
         if (t >= zs + 2 && t < ze + 2 && own) {
@@ -472,24 +475,31 @@ struct FusedPlan {
     using FT = FusedTile<T, PT, QS>;
     using TL = typename FT::TL;
 
-    // two-point kernel: fp16 / fp32 compute (all of WC, T, PT <= 4 bytes)
-    // (packed fp32 measured slower than scalar fp32 at 2 CTAs/SM: the
-    // contraction barrier costs an ALU op per multiply; fp16 pairs are native)
-    static constexpr bool PAIR = sizeof(T) == 2 && sizeof(WC) <= 4 && sizeof(PT) <= 4;
 #ifndef MPFD_STAGE2
 #define MPFD_STAGE2 1
 #endif
-    // STAGE2: one 512-thread CTA per SM on a 64 x 16 tile with the next
-    // plane's Q staged by cp.async; otherwise two 256-thread CTAs on 64 x 8
-    // with a register prefetch
-    static constexpr size_t SMEM2S =
-        ((FusedSmem<Tile<64, 16>, T, PT>::total + 15) & ~(size_t)15) + (size_t)5 * Tile<64, 16>::R4N * sizeof(QS);
-    static constexpr bool STAGE2 = MPFD_STAGE2 != 0 && SMEM2S <= 232448;
-    using TL2 = typename std::conditional<STAGE2, Tile<64, 16>, Tile<64, 8>>::type;
+#ifndef MPFD_PAIR32
+#define MPFD_PAIR32 1
+#endif
+    // two-point kernel: fp16 compute (HADD2/HMUL2) and, where the staged
+    // rings fit, fp32 compute (FADD2 / FFMA2-with-opaque-zero products).
+    // fp16: one 512-thread CTA per SM on a 64 x 16 tile (two 256-thread CTAs
+    // on 64 x 8 with a register prefetch when the rings do not fit);
+    // fp32: one 256-thread CTA per SM on a 32 x 16 tile.  Staged tiles copy
+    // the next plane's Q into shared memory by cp.async.
+    template <class TLx>
+    static constexpr size_t staged_smem() {
+        return ((FusedSmem<TLx, T, PT>::total + 15) & ~(size_t)15) + (size_t)5 * TLx::R4N * sizeof(QS);
+    }
+    using TLS2 = typename std::conditional<sizeof(T) == 2, Tile<64, 16>, Tile<32, 16>>::type;
+    static constexpr bool STAGE2 = MPFD_STAGE2 != 0 && staged_smem<TLS2>() <= 232448;
+    static constexpr bool PAIR16 = sizeof(T) == 2 && sizeof(WC) <= 4 && sizeof(PT) <= 4;
+    static constexpr bool PAIR32 =
+        MPFD_PAIR32 != 0 && STAGE2 && sizeof(T) == 4 && sizeof(WC) == 4 && sizeof(PT) == 4;
+    static constexpr bool PAIR = PAIR16 || PAIR32;
+    using TL2 = typename std::conditional<STAGE2, TLS2, Tile<64, 8>>::type;
     static constexpr int MINB2 = STAGE2 ? 1 : ((sizeof(T) == 2 && sizeof(PT) == 2) ? 2 : 1);
-    static constexpr size_t SMEM2 =
-        STAGE2 ? ((FusedSmem<TL2, T, PT>::total + 15) & ~(size_t)15) + (size_t)5 * TL2::R4N * sizeof(QS)
-               : FusedSmem<TL2, T, PT>::total;
+    static constexpr size_t SMEM2 = STAGE2 ? staged_smem<TL2>() : FusedSmem<TL2, T, PT>::total;
 
     static int z_range(const Geo& g, int nz, int tx, int ty, int minb) {
         // z planes per CTA: about 8 waves of CTAs over the 148 SMs, but at
@@ -570,7 +580,7 @@ struct FusedPlan {
         // compiled with its term mask fixed; any other split runs the generic
         // runtime-masked kernel (same arithmetic, physics.cpp:93-155)
         constexpr unsigned kBlaisdell = 0x25u;
-        if (rc.nz == kBlaisdell) {
+        if (rc.nz == kBlaisdell && rc.viscous) {
             if (staged) go<true, kBlaisdell>(a, st);
             else go<false, kBlaisdell>(a, st);
         } else {
