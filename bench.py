@@ -282,7 +282,7 @@ def main():
             "b_alg_bytes_per_pt": b_alg(preset),
             "b_alg_frac": rate * b_alg(preset) / 1e9 / hbm,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic_lookup(preset, n, fused),
+                         "frac": achieved / hbm, "traffic": traffic_lookup(preset, nloc, fused),
                          "kernel": kname, "avg_ms_per_substep": avg_ms,
                          "bytes_per_pt_per_launch": per_pt, "peak_source": peak_src},
             "kernel_ms": {"dominant": kms[0], "rk": kms[1], "halo": kms[2], "other": kms[3]},
@@ -353,13 +353,17 @@ def main():
     return 0
 
 
-def traffic_lookup(preset, n, fused):
-    """dram bytes per launch from the committed ncu capture, if any."""
+def traffic_lookup(preset, npts, fused):
+    """DRAM bytes per launch of the dominant kernel: the per-point
+    dram__bytes_read.sum + dram__bytes_write.sum of the committed ncu --set
+    full capture (profiles/ncu_traffic.json, 256^3) times this launch's
+    points; None when no capture exists for this preset and path."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(f"{preset}/{n}/{'fused' if fused else 'staged'}")
+        v = d.get(f"{preset}/{'fused' if fused else 'staged'}/bytes_per_pt")
+        return None if v is None else v * npts
     except Exception:
         return None
 
