@@ -136,6 +136,33 @@ __device__ __forceinline__ T ring_grad(const PT* const pl[5], int q, int i, int 
     return cvt<T>(round_kind<WC>(sc.kind[i == 3 ? 9 + j : i * 3 + j], v));
 }
 
+// Rare path of the fused kernels' guards, out of line so the common path
+// carries none of its index arithmetic.  Records the first-in-scan-order
+// events (reduce.cpp:57-81, physics.cpp:309-312) of this thread's point(s)
+// on local plane c; PW points per thread along x.  bits: 1/2 residual lane
+// 0/1 non-finite, 4/8 state lane 0/1 non-finite, 16/32 density lane 0/1.
+template <class TL, int PW>
+__device__ __noinline__ void report_point(const Geo g, DevDiv* d, int iter, int sub, int c, int comp,
+                                          unsigned bits) {
+    constexpr int TXT = TL::TX / PW;
+    const int x = blockIdx.x * TL::TX + PW * ((int)threadIdx.x % TXT);
+    const int y = blockIdx.y * TL::TY + (int)threadIdx.x / TXT;
+    const unsigned long long gi = ((unsigned long long)(g.z0 + c) * g.ny + y) * g.nx + x;
+    if (bits & 1u) record_div(d, 1, comp, gi, iter, sub);
+    if (bits & 2u) record_div(d, 1, comp, gi + 1, iter, sub);
+    if (bits & 4u) record_div(d, 2, comp, gi, iter, sub);
+    if (bits & 8u) record_div(d, 2, comp, gi + 1, iter, sub);
+}
+// density signal of a rim point: element index e of the R4 box, PW lanes
+template <class TL>
+__device__ __noinline__ void report_rho(const Geo g, DevDiv* d, int iter, int sub, int t, int e, unsigned bits) {
+    const int ry = e / TL::R4X, rx = e - ry * TL::R4X;
+    const unsigned long long gi = ((unsigned long long)(g.z0 + t) * g.ny + (blockIdx.y * TL::TY - 4 + ry)) * g.nx +
+                                  (blockIdx.x * TL::TX - 4 + rx);
+    if (bits & 1u) record_div(d, 0, 0, gi, iter, sub);
+    if (bits & 2u) record_div(d, 0, 0, gi + 1, iter, sub);
+}
+
 // operands of the stage update at one point, loaded ahead of their use
 // (the loads' latency overlaps the residual arithmetic)
 template <class QS, class TS>
@@ -170,7 +197,7 @@ __device__ __forceinline__ void rk_prefetch_l2(const FusedArgs& a, int comp, int
     asm volatile("prefetch.global.L2 [%0];" ::"l"((const QS*)a.qin + iq));
 }
 
-template <class QS, class TS, class RS, class TC, class QC>
+template <class QS, class TS, class RS, class TC, class QC, class TL>
 __device__ __forceinline__ void rk_point(const FusedArgs& a, int comp, int c, long long o, RS rs,
                                          RkIn<QS, TS> in, int x, int y) {
     const Geo& g = a.g;
@@ -260,6 +287,7 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
     using PFT = typename std::conditional<std::is_same<WC, T>::value, T, QS>::type;
 #endif
     int rim_off[KPF];
+    unsigned inner_mask = 0;  // bit k: rim point k is an owned interior point
     PFT pf[STAGE ? 1 : KPF][5];
     QS* Sg = (QS*)(smem_raw + ((SM::total + 15) & ~(size_t)15));  // STAGE: [5][R4N] raw Q of the next plane
     const bool fastwrap = g.nx >= TL::TX + 8 && g.ny >= TL::TY + 8;
@@ -280,6 +308,9 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             if (yy < 0) yy += g.ny;
         }
         rim_off[k] = yy * g.nx + xx;
+        if (rx >= 4 && rx < TL::TX + 4 && ry >= 4 && ry < TL::TY + 4 && x0 - 4 + rx < g.nx && y0 - 4 + ry < g.ny &&
+            tid + k * TL::NT < TL::R4N)
+            inner_mask |= 1u << k;
         if constexpr (!STAGE) {
             const QS* qp = qin + (long long)(zs - 4 + kHalo) * 5 * g.plane + rim_off[k];
 #pragma unroll
@@ -347,12 +378,15 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             const WC ux = pv.ux, uy = pv.uy, uz = pv.uz, pr = pv.pr, Tv = pv.Tv;
             PT* pp = Pr + slot * TL::R4N + i;
             constexpr int FS = TL::NRING * TL::R4N;
-            pp[0] = cvt<PT>(RK1<WC>(a.pc.round, a.pc.kind[0], ux));
-            pp[FS] = cvt<PT>(RK1<WC>(a.pc.round, a.pc.kind[1], uy));
-            pp[2 * FS] = cvt<PT>(RK1<WC>(a.pc.round, a.pc.kind[2], uz));
-            pp[3 * FS] = cvt<PT>(RK1<WC>(a.pc.round, a.pc.kind[4], Tv));
+            // the fixed-split instance runs only where the primitive store
+            // rounding (physics.cpp:323-327) is the identity
+            const int rnd = SPL != 0 ? 0 : a.pc.round;
+            pp[0] = cvt<PT>(RK1<WC>(rnd, a.pc.kind[0], ux));
+            pp[FS] = cvt<PT>(RK1<WC>(rnd, a.pc.kind[1], uy));
+            pp[2 * FS] = cvt<PT>(RK1<WC>(rnd, a.pc.kind[2], uz));
+            pp[3 * FS] = cvt<PT>(RK1<WC>(rnd, a.pc.kind[4], Tv));
             if (rx >= 2 && rx < TL::TX + 6 && ry >= 2 && ry < TL::TY + 6) {
-                Ppr[slot * TL::R2N + (ry - 2) * TL::R2X + (rx - 2)] = cvt<PT>(RK1<WC>(a.pc.round, a.pc.kind[3], pr));
+                Ppr[slot * TL::R2N + (ry - 2) * TL::R2X + (rx - 2)] = cvt<PT>(RK1<WC>(rnd, a.pc.kind[3], pr));
                 T* qq = Qr + slot * TL::R2N + (ry - 2) * TL::R2X + (rx - 2);
                 constexpr int QF = TL::NRING * TL::R2N;
                 qq[0] = cvt<T>(q0);
@@ -363,8 +397,7 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             }
             // density signal (physics.cpp:309-312): interior points of this
             // CTA, planes it owns, exactly once
-            if (t >= zs && t < ze && rx >= 4 && rx < TL::TX + 4 && ry >= 4 && ry < TL::TY + 4 &&
-                x0 - 4 + rx < g.nx && y0 - 4 + ry < g.ny) {
+            if (((inner_mask >> k) & 1u) && t >= zs && t < ze) {
                 if (!Op<WC>::positive(rho) || nonfinite(rho)) {
                     const unsigned long long gi =
                         ((unsigned long long)(g.z0 + t) * g.ny + (y0 - 4 + ry)) * g.nx + (x0 - 4 + rx);
@@ -478,8 +511,8 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             T rw_, rE;
             residual_late<T>(c, dfr[0], cw, tz, hz, rw_, rE);
             const int cpl = t - 4;
-            rk_point<QS, TS, RS, TC, QC>(a, 3, cpl, o, cvt<RS>(rw_), ind[0], x, y);
-            rk_point<QS, TS, RS, TC, QC>(a, 4, cpl, o, cvt<RS>(rE), ind[1], x, y);
+            rk_point<QS, TS, RS, TC, QC, TL>(a, 3, cpl, o, cvt<RS>(rw_), ind[0], x, y);
+            rk_point<QS, TS, RS, TC, QC, TL>(a, 4, cpl, o, cvt<RS>(rE), ind[1], x, y);
         }
         // deferred window: dfr[0] plane t-3, dfr[1] plane t-2 after this step
         dfr[0] = dfr[1];  // (unused until phase D first runs at t = zs + 4)
@@ -508,7 +541,7 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
 #endif
 #pragma unroll
             for (int comp = 0; comp < 3; ++comp)
-                rk_point<QS, TS, RS, TC, QC>(a, comp, cpl, o, cvt<RS>(out[comp]), inc[comp], x, y);
+                rk_point<QS, TS, RS, TC, QC, TL>(a, comp, cpl, o, cvt<RS>(out[comp]), inc[comp], x, y);
         }
         if constexpr (STAGE) cp_async_wait_all();
         __syncthreads();

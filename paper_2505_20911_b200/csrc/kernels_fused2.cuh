@@ -98,7 +98,7 @@ __device__ __forceinline__ RkIn2<QS, TS> rk_load2(const FusedArgs& a, int comp, 
     return v;
 }
 
-template <class QS, class TS, class RS, class TC, class QC>
+template <class QS, class TS, class RS, class TC, class QC, class TL>
 __device__ __forceinline__ void rk_pair(const FusedArgs& a, int comp, int c, long long o,
                                         typename V2<RS>::type rs, RkIn2<QS, TS> in, int x, int y) {
     using TC2 = typename V2<TC>::type;
@@ -119,11 +119,18 @@ __device__ __forceinline__ void rk_pair(const FusedArgs& a, int comp, int c, lon
     stv<QS>((QS*)a.qout + iq, ns);
     if (a.write_r) stv<RS>((RS*)a.r + ir, rs);
     if (nonfinite2(rs) | nonfinite2(ns)) {
-        const unsigned long long gi = ((unsigned long long)(g.z0 + c) * g.ny + y) * g.nx + x;
-        if (nonfinite(lo(rs))) record_div(a.div, 1, comp, gi, a.iter, a.sub);
-        if (nonfinite(hi(rs))) record_div(a.div, 1, comp, gi + 1, a.iter, a.sub);
-        if (nonfinite(lo(ns))) record_div(a.div, 2, comp, gi, a.iter, a.sub);
-        if (nonfinite(hi(ns))) record_div(a.div, 2, comp, gi + 1, a.iter, a.sub);
+        const unsigned bits = (nonfinite(lo(rs)) ? 1u : 0u) | (nonfinite(hi(rs)) ? 2u : 0u) |
+                              (nonfinite(lo(ns)) ? 4u : 0u) | (nonfinite(hi(ns)) ? 8u : 0u);
+        // out of line for fp16 residuals (measured faster); inline otherwise
+        if constexpr (sizeof(RS) == 2) {
+            report_point<TL, 2>(g, a.div, a.iter, a.sub, c, comp, bits);
+        } else {
+            const unsigned long long gi = ((unsigned long long)(g.z0 + c) * g.ny + y) * g.nx + x;
+            if (bits & 1u) record_div(a.div, 1, comp, gi, a.iter, a.sub);
+            if (bits & 2u) record_div(a.div, 1, comp, gi + 1, a.iter, a.sub);
+            if (bits & 4u) record_div(a.div, 2, comp, gi, a.iter, a.sub);
+            if (bits & 8u) record_div(a.div, 2, comp, gi + 1, a.iter, a.sub);
+        }
     }
 }
 
@@ -185,6 +192,10 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
 #endif
     using PF2 = typename V2<PFS>::type;
     int rim_off[KPF];
+    // per-thread rim descriptors, constant over the z-march: bits 0-12 the
+    // pair's element index in a P-ring plane, 13-25 its index in an R2 plane,
+    // 26 inside the R2 box, 27 an owned interior point (density signal)
+    unsigned rinfo[KPF];
     PF2 pf[STAGE ? 1 : KPF][5];
     using QS2 = typename V2<QS>::type;
     QS* Sg = (QS*)(smem_raw + ((SM::total + 15) & ~(size_t)15));  // STAGE: [5][R4N] raw Q of the next plane
@@ -206,6 +217,13 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
             if (yy < 0) yy += g.ny;
         }
         rim_off[k] = yy * g.nx + xx;
+        {
+            const bool in2 = rx >= 2 && rx < TL::TX + 6 && ry >= 2 && ry < TL::TY + 6;
+            const bool inner = rx >= 4 && rx < TL::TX + 4 && ry >= 4 && ry < TL::TY + 4 && x0 - 4 + rx < g.nx &&
+                               y0 - 4 + ry < g.ny;
+            rinfo[k] = (unsigned)(ry * TL::R4X + rx) | ((unsigned)(in2 ? (ry - 2) * TL::R2X + (rx - 2) : 0) << 13) |
+                       (in2 ? 1u << 26 : 0u) | (inner ? 1u << 27 : 0u);
+        }
         if constexpr (!STAGE) {
             const QS* qp = qin + (long long)(zs - 4 + kHalo) * 5 * g.plane + rim_off[k];
 #pragma unroll
@@ -255,7 +273,7 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
         for (int k = 0; k < KPF; ++k) {
             const int i = tid + k * NT;
             if (i >= R4NP) break;
-            const int ry = i / R4P, rx = 2 * (i - ry * R4P);
+            const unsigned ri = rinfo[k];
             PF2 q0, q1, q2, q3, q4;
             if constexpr (STAGE) {
                 const QS* sp = Sg + 2 * i;
@@ -268,19 +286,20 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
                 const int kk = STAGE ? 0 : k;
                 q0 = pf[kk][0], q1 = pf[kk][1], q2 = pf[kk][2], q3 = pf[kk][3], q4 = pf[kk][4];
             }
-            using O = Op<WC2>;
             const WC2 rho = cvt<WC2>(q0);
             const PrimOut<WC2> pv = PrimCalc<WC2>::run(rho, cvt<WC2>(q1), cvt<WC2>(q2), cvt<WC2>(q3), cvt<WC2>(q4), half, gm1, gM2);
-            const WC2 ux = pv.ux, uy = pv.uy, uz = pv.uz, pr = pv.pr, Tv = pv.Tv;
+            // primitive stores round to each field's storage (physics.cpp:323-327);
+            // the fixed-split instance runs only where that is the identity
+            const int rnd = SPL != 0 ? 0 : a.pc.round;
             constexpr int FS = TL::NRING * TL::R4N;
-            PT* pp = Pr + slot * TL::R4N + ry * TL::R4X + rx;
-            stv<PT>(pp, cvt<PT2>(RKV<WC2>(a.pc.round, a.pc.kind[0], ux)));
-            stv<PT>(pp + FS, cvt<PT2>(RKV<WC2>(a.pc.round, a.pc.kind[1], uy)));
-            stv<PT>(pp + 2 * FS, cvt<PT2>(RKV<WC2>(a.pc.round, a.pc.kind[2], uz)));
-            stv<PT>(pp + 3 * FS, cvt<PT2>(RKV<WC2>(a.pc.round, a.pc.kind[4], Tv)));
-            if (rx >= 2 && rx < TL::TX + 6 && ry >= 2 && ry < TL::TY + 6) {
-                const int q2i = (ry - 2) * TL::R2X + (rx - 2);
-                stv<PT>(Ppr + slot * TL::R2N + q2i, cvt<PT2>(RKV<WC2>(a.pc.round, a.pc.kind[3], pr)));
+            PT* pp = Pr + slot * TL::R4N + (ri & 0x1FFFu);
+            stv<PT>(pp, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[0], pv.ux)));
+            stv<PT>(pp + FS, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[1], pv.uy)));
+            stv<PT>(pp + 2 * FS, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[2], pv.uz)));
+            stv<PT>(pp + 3 * FS, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[4], pv.Tv)));
+            if (ri & (1u << 26)) {
+                const int q2i = (int)((ri >> 13) & 0x1FFFu);
+                stv<PT>(Ppr + slot * TL::R2N + q2i, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[3], pv.pr)));
                 T* qq = Qr + slot * TL::R2N + q2i;
                 constexpr int QF = TL::NRING * TL::R2N;
                 stv<T>(qq, cvt<T2>(q0));
@@ -289,16 +308,22 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
                 stv<T>(qq + 3 * QF, cvt<T2>(q3));
                 stv<T>(qq + 4 * QF, cvt<T2>(q4));
             }
-            if (t >= zs && t < ze && rx >= 4 && rx < TL::TX + 4 && ry >= 4 && ry < TL::TY + 4 &&
-                x0 - 4 + rx < g.nx && y0 - 4 + ry < g.ny) {
+            // density signal (physics.cpp:309-312): owned interior points,
+            // planes this CTA owns, exactly once
+            if ((ri & (1u << 27)) && t >= zs && t < ze) {
                 using OS = Op<WC>;
                 const bool b0 = !OS::positive(lo(rho)) || nonfinite(lo(rho));
                 const bool b1 = !OS::positive(hi(rho)) || nonfinite(hi(rho));
                 if (b0 | b1) {
-                    const unsigned long long gi =
-                        ((unsigned long long)(g.z0 + t) * g.ny + (y0 - 4 + ry)) * g.nx + (x0 - 4 + rx);
-                    if (b0) record_div(a.div, 0, 0, gi, a.iter, a.sub);
-                    if (b1) record_div(a.div, 0, 0, gi + 1, a.iter, a.sub);
+                    if constexpr (sizeof(T) == 2) {
+                        report_rho<TL>(g, a.div, a.iter, a.sub, t, (int)(ri & 0x1FFFu), (b0 ? 1u : 0u) | (b1 ? 2u : 0u));
+                    } else {
+                        const int e = (int)(ri & 0x1FFFu), ry = e / TL::R4X, rx = e - ry * TL::R4X;
+                        const unsigned long long gi =
+                            ((unsigned long long)(g.z0 + t) * g.ny + (y0 - 4 + ry)) * g.nx + (x0 - 4 + rx);
+                        if (b0) record_div(a.div, 0, 0, gi, a.iter, a.sub);
+                        if (b1) record_div(a.div, 0, 0, gi + 1, a.iter, a.sub);
+                    }
                 }
             }
             if constexpr (!STAGE) {
@@ -404,8 +429,8 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
             }
             T2 rw_, rE;
             residual_late<T2>(c, dfr[0], cw, tz, hz, rw_, rE);
-            rk_pair<QS, TS, RS, TC, QC>(a, 3, t - 4, o, cvt<RS2>(rw_), ind[0], x, y);
-            rk_pair<QS, TS, RS, TC, QC>(a, 4, t - 4, o, cvt<RS2>(rE), ind[1], x, y);
+            rk_pair<QS, TS, RS, TC, QC, TL>(a, 3, t - 4, o, cvt<RS2>(rw_), ind[0], x, y);
+            rk_pair<QS, TS, RS, TC, QC, TL>(a, 4, t - 4, o, cvt<RS2>(rE), ind[1], x, y);
         }
         dfr[0] = dfr[1];  // (unused until phase D first runs at t = zs + 4)
 
@@ -432,7 +457,7 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
 #endif
 #pragma unroll
             for (int comp = 0; comp < 3; ++comp)
-                rk_pair<QS, TS, RS, TC, QC>(a, comp, t - 2, o, cvt<RS2>(out[comp]), inc[comp], x, y);
+                rk_pair<QS, TS, RS, TC, QC, TL>(a, comp, t - 2, o, cvt<RS2>(out[comp]), inc[comp], x, y);
         }
         if constexpr (STAGE) cp_async_wait_all();
         __syncthreads();
@@ -442,6 +467,12 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
         sl[4] = s0;
     }
 }
+
+}  // namespace mpfd_b200
+
+#include "kernels_ws.cuh"
+
+namespace mpfd_b200 {
 
 template <int K>
 struct KT;
@@ -510,8 +541,33 @@ struct FusedPlan {
         return std::max(lz, std::min(16, nz));
     }
 
+#ifndef MPFD_WS
+#define MPFD_WS 0
+#endif
+    // warp-specialised kernel (kernels_ws.cuh): fp16 64x12 tile with 4
+    // producer warps, fp32 32x12 with 2
+    using TLW = typename std::conditional<sizeof(T) == 2, TileWS<64, 12>, TileWS<32, 12>>::type;
+    static constexpr int NPW = sizeof(T) == 2 ? 4 : 2;
+    static constexpr bool WS = MPFD_WS != 0 && PAIR && WsSmem<TLW, T, PT, QS>::total <= 232448;
+
     template <bool ST, unsigned SPL>
     static void go(FusedArgs a, cudaStream_t st) {
+        if constexpr (WS) {
+            if (a.g.nx % 2 == 0) {
+                auto kern = k_fused_ws<QS, TS, RS, PT, WC, T, TC, QC, ST, TLW, NPW, SPL>;
+                constexpr size_t smem = WsSmem<TLW, T, PT, QS>::total;
+                static bool attr = false;
+                if (!attr) {
+                    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                    attr = true;
+                }
+                a.lz = z_range(a.g, a.zhi - a.zlo, TLW::TX, TLW::TY, 1);
+                const dim3 grid((a.g.nx + TLW::TX - 1) / TLW::TX, (a.g.ny + TLW::TY - 1) / TLW::TY,
+                                (a.zhi - a.zlo + a.lz - 1) / a.lz);
+                kern<<<grid, NPW * 32 + TLW::NT / 2, smem, st>>>(a);
+                return;
+            }
+        }
         if constexpr (PAIR) {
             if (a.g.nx % 2 == 0) {
             auto kern = k_fused2<QS, TS, RS, PT, WC, T, TC, QC, ST, TL2, MINB2, SPL, STAGE2>;
@@ -580,7 +636,7 @@ struct FusedPlan {
         // compiled with its term mask fixed; any other split runs the generic
         // runtime-masked kernel (same arithmetic, physics.cpp:93-155)
         constexpr unsigned kBlaisdell = 0x25u;
-        if (rc.nz == kBlaisdell && rc.viscous) {
+        if (rc.nz == kBlaisdell && rc.viscous && pc.round == 0) {
             if (staged) go<true, kBlaisdell>(a, st);
             else go<false, kBlaisdell>(a, st);
         } else {

@@ -1,0 +1,346 @@
+// kernels_ws.cuh -- warp-specialised fused substep kernel (two x-points per
+// consumer thread).  Same arithmetic as k_fused2 (kernels_fused2.cuh), so the
+// results are bitwise the reference's; only the schedule differs.
+//
+// A CTA owns a TX x TY column tile and a z-range and marches up in z, as in
+// k_fused2, but its warps have two roles that run concurrently:
+//   producers (NPW warps): phase A -- Q of plane p from the cp.async staging
+//     buffer -> primitives on the 4-point rim and Q (narrowed) on the 2-point
+//     rim into 6-slot rings -- and phase B on the cross-shaped rim of plane
+//     p-2 (level-2 viscous fields), plus the cp.async copy of plane p+1;
+//   consumers (TX*TY/2 threads, one point pair each): phase B at their own
+//     pair (level-2 fields + the z-register windows), then the late residual
+//     of plane c-2 and the early residual of plane c, and their RK updates.
+// Roles hand planes to each other through named barriers (bar.arrive by the
+// signalling side, bar.sync by the waiting side; ids alternate with the plane
+// parity so consecutive hand-offs never share a barrier):
+//   FULL(p)    producers arrive after A(p); consumers wait before B(p-2)
+//   LREADY(c)  producers arrive after the rim part of B(c); consumers wait
+//              (all of them) before the residual of plane c reads level-2
+//              values of their neighbours
+//   EMPTY(c)   consumers arrive after C(c); producers wait before A(c+4),
+//              which overwrites the ring slot of plane c-2, and before the rim
+//              part of B(c+2), which overwrites the level-2 buffer of c
+// With 6 ring slots, A(p) never overwrites a plane that an unfinished residual
+// reads, so phase A of later planes overlaps the residual of earlier ones and
+// the FP16/FP32 work of the residual interleaves with the division and
+// conversion work of the primitives on every SM sub-partition.
+#pragma once
+
+#include "kernels_fused2.cuh"
+
+namespace mpfd_b200 {
+
+template <int TX_, int TY_>
+struct TileWS {
+    static constexpr int TX = TX_, TY = TY_, NT = TX * TY;
+    static constexpr int R4X = TX + 8, R4Y = TY + 8, R4N = R4X * R4Y;
+    static constexpr int R2X = TX + 4, R2Y = TY + 4, R2N = R2X * R2Y;
+    static constexpr int NRING = 6;
+};
+
+// shared-memory carve-up: 6-slot rings, a double level-2 buffer, staging
+template <class TL, class RCt, class PT, class QS>
+struct WsSmem {
+    static constexpr size_t p_bytes = (size_t)4 * TL::NRING * TL::R4N * sizeof(PT);
+    static constexpr size_t pp_bytes = (size_t)TL::NRING * TL::R2N * sizeof(PT);
+    static constexpr size_t q_bytes = (size_t)5 * TL::NRING * TL::R2N * sizeof(RCt);
+    static constexpr size_t l_bytes = (size_t)2 * 5 * TL::R2N * sizeof(RCt);
+    static constexpr size_t s_off = (p_bytes + pp_bytes + q_bytes + l_bytes + 15) & ~(size_t)15;
+    static constexpr size_t total = s_off + (size_t)5 * TL::R4N * sizeof(QS);
+};
+
+__device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// the arriving side's shared-memory writes are ordered before its arrival
+__device__ __forceinline__ void nb_arrive(int id, int n) {
+    __threadfence_block();
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+enum WsBar { WS_PROD = 1, WS_FULL = 2, WS_LREADY = 4, WS_EMPTY = 6 };  // +0/+1 by plane parity
+
+__device__ __forceinline__ int ring_slot(int p) { return (p + 12) % 6; }
+
+template <class QS, class TS, class RS, class PT, class WC, class T, class TC, class QC, bool STAGED, class TL,
+          int NPW, unsigned SPL>
+__global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs a) {
+    if (a.div->flag && (a.div->iter != a.iter || a.div->sub != a.sub)) return;
+    using T2 = typename V2<T>::type;
+    using WC2 = typename V2<WC>::type;
+    using PT2 = typename V2<PT>::type;
+    using RS2 = typename V2<RS>::type;
+    using QS2 = typename V2<QS>::type;
+    constexpr int NP = NPW * 32;        // producer threads
+    constexpr int NC = TL::NT / 2;      // consumer threads (one pair each)
+    constexpr int NALL = NP + NC;
+    constexpr int TXP = TL::TX / 2;
+    constexpr int R4P = TL::R4X / 2;
+    constexpr int R4NP = TL::R4N / 2;
+    using SM = WsSmem<TL, T, PT, QS>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PT* Pr = (PT*)smem_raw;
+    PT* Ppr = (PT*)(smem_raw + SM::p_bytes);
+    T* Qr = (T*)(smem_raw + SM::p_bytes + SM::pp_bytes);
+    T* Lbuf = (T*)(smem_raw + SM::p_bytes + SM::pp_bytes + SM::q_bytes);
+    QS* Sg = (QS*)(smem_raw + SM::s_off);
+
+    const Geo& g = a.g;
+    const int tid = threadIdx.x;
+    const int x0 = blockIdx.x * TL::TX, y0 = blockIdx.y * TL::TY;
+    const int zs = a.zlo + blockIdx.z * a.lz;
+    const int ze = min(zs + a.lz, a.zhi);
+
+    RC<T2> c(a.kb, a.rc);
+    if constexpr (SPL != 0) c.viscous = 1;
+    const WC2 rw = kget<WC2>(a.kb[K_R_STAGE]);
+    const QS* qin = (const QS*)a.qin;
+    constexpr int PF = TL::NRING * TL::R4N;
+
+    if (tid < NP) {
+        // ======================= producers ====================================
+        const int ptid = tid;
+        const WC2 half = kget<WC2>(a.kb[K_HALF]), gm1 = kget<WC2>(a.kb[K_GM1]), gM2 = kget<WC2>(a.kb[K_GM2]);
+        constexpr int KPF = (R4NP + NP - 1) / NP;
+        int rim_off[KPF];
+        unsigned rinfo[KPF];
+        const bool fastwrap = g.nx >= TL::TX + 8 && g.ny >= TL::TY + 8;
+#pragma unroll
+        for (int k = 0; k < KPF; ++k) {
+            const int i = min(ptid + k * NP, R4NP - 1);
+            const int ry = i / R4P, rx = 2 * (i - ry * R4P);
+            int xx = x0 - 4 + rx, yy = y0 - 4 + ry;
+            if (fastwrap) {
+                xx += xx < 0 ? g.nx : 0;
+                xx -= xx >= g.nx ? g.nx : 0;
+                yy += yy < 0 ? g.ny : 0;
+                yy -= yy >= g.ny ? g.ny : 0;
+            } else {
+                xx %= g.nx;
+                if (xx < 0) xx += g.nx;
+                yy %= g.ny;
+                if (yy < 0) yy += g.ny;
+            }
+            rim_off[k] = yy * g.nx + xx;
+            const bool in2 = rx >= 2 && rx < TL::TX + 6 && ry >= 2 && ry < TL::TY + 6;
+            const bool inner = rx >= 4 && rx < TL::TX + 4 && ry >= 4 && ry < TL::TY + 4 && x0 - 4 + rx < g.nx &&
+                               y0 - 4 + ry < g.ny;
+            rinfo[k] = (unsigned)(ry * TL::R4X + rx) | ((unsigned)(in2 ? (ry - 2) * TL::R2X + (rx - 2) : 0) << 13) |
+                       (in2 ? 1u << 26 : 0u) | (inner ? 1u << 27 : 0u);
+        }
+        // each producer thread copies exactly the staging entries it reads
+        auto stage_issue = [&](int p) {
+            const QS* qb = qin + (long long)(p + kHalo) * 5 * g.plane;
+#pragma unroll
+            for (int k = 0; k < KPF; ++k) {
+                const int i = ptid + k * NP;
+                if (i >= R4NP) break;
+#pragma unroll
+                for (int cc = 0; cc < 5; ++cc)
+                    cp_async<2 * sizeof(QS)>(Sg + cc * TL::R4N + 2 * i, qb + cc * g.plane + rim_off[k]);
+            }
+            cp_async_commit();
+        };
+        stage_issue(zs - 4);
+
+        for (int p = zs - 4; p < ze + 4; ++p) {
+            // A(p) overwrites the slot of plane p-6 (last read by C(p-4)); the
+            // rim part of B(p-2) below overwrites the level-2 buffer of p-4
+            if (p >= zs + 2) nb_sync(WS_EMPTY + (p & 1), NALL);
+            cp_async_wait_all();
+            const int slot = ring_slot(p);
+#pragma unroll
+            for (int k = 0; k < KPF; ++k) {
+                const int i = ptid + k * NP;
+                if (i >= R4NP) break;
+                const unsigned ri = rinfo[k];
+                const QS* sp = Sg + 2 * i;
+                const QS2 q0 = ldv<QS>(sp), q1 = ldv<QS>(sp + TL::R4N), q2 = ldv<QS>(sp + 2 * TL::R4N),
+                          q3 = ldv<QS>(sp + 3 * TL::R4N), q4 = ldv<QS>(sp + 4 * TL::R4N);
+                const WC2 rho = cvt<WC2>(q0);
+                const PrimOut<WC2> pv =
+                    PrimCalc<WC2>::run(rho, cvt<WC2>(q1), cvt<WC2>(q2), cvt<WC2>(q3), cvt<WC2>(q4), half, gm1, gM2);
+                if (p + 1 < ze + 4) {
+                    // this thread's staging entries were consumed (their loads
+                    // fed the primitives above): copy plane p+1 into them
+                    const QS* qb = qin + (long long)(p + 1 + kHalo) * 5 * g.plane + rim_off[k];
+#pragma unroll
+                    for (int cc = 0; cc < 5; ++cc) cp_async<2 * sizeof(QS)>(Sg + cc * TL::R4N + 2 * i, qb + cc * g.plane);
+                }
+                const int rnd = SPL != 0 ? 0 : a.pc.round;
+                PT* pp = Pr + slot * TL::R4N + (ri & 0x1FFFu);
+                stv<PT>(pp, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[0], pv.ux)));
+                stv<PT>(pp + PF, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[1], pv.uy)));
+                stv<PT>(pp + 2 * PF, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[2], pv.uz)));
+                stv<PT>(pp + 3 * PF, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[4], pv.Tv)));
+                if (ri & (1u << 26)) {
+                    const int q2i = (int)((ri >> 13) & 0x1FFFu);
+                    stv<PT>(Ppr + slot * TL::R2N + q2i, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[3], pv.pr)));
+                    T* qq = Qr + slot * TL::R2N + q2i;
+                    constexpr int QF = TL::NRING * TL::R2N;
+                    stv<T>(qq, cvt<T2>(q0));
+                    stv<T>(qq + QF, cvt<T2>(q1));
+                    stv<T>(qq + 2 * QF, cvt<T2>(q2));
+                    stv<T>(qq + 3 * QF, cvt<T2>(q3));
+                    stv<T>(qq + 4 * QF, cvt<T2>(q4));
+                }
+                if ((ri & (1u << 27)) && p >= zs && p < ze) {
+                    using OS = Op<WC>;
+                    const bool b0 = !OS::positive(lo(rho)) || nonfinite(lo(rho));
+                    const bool b1 = !OS::positive(hi(rho)) || nonfinite(hi(rho));
+                    if (b0 | b1) report_rho<TL>(g, a.div, a.iter, a.sub, p, (int)(ri & 0x1FFFu),
+                                                (b0 ? 1u : 0u) | (b1 ? 2u : 0u));
+                }
+            }
+            cp_async_commit();
+            if (p >= zs) nb_arrive(WS_FULL + (p & 1), NALL);
+            // ---- rim part of B(p-2): needs A(p) of every producer ----
+            const int cpl = p - 2;
+            if (c.viscous && cpl >= zs - 2 && cpl < ze + 2) {
+                nb_sync(WS_PROD, NP);
+                const PT* plp[5];
+#pragma unroll
+                for (int i = 0; i < 5; ++i) plp[i] = Pr + ring_slot(cpl - 2 + i) * TL::R4N;
+                T* Lb = Lbuf + (cpl & 1) * 5 * TL::R2N;
+                constexpr int NXR = 2 * TL::TY, NYR = 4 * TXP;
+                for (int k = ptid; k < NXR + NYR; k += NP) {
+                    int rx, ry, dir;
+                    if (k < NXR) {
+                        const int col = k / TL::TY;
+                        ry = k - col * TL::TY;
+                        rx = col == 0 ? -2 : TL::TX;
+                        dir = 0;
+                    } else {
+                        const int kk = k - NXR;
+                        const int row = kk / TXP;
+                        rx = 2 * (kk - row * TXP);
+                        ry = row < 2 ? row - 2 : TL::TY + row - 2;
+                        dir = 1;
+                    }
+                    const int q4 = (ry + 4) * TL::R4X + rx + 4;
+                    const int q2 = (ry + 2) * TL::R2X + rx + 2;
+                    T2 G[9], u[3];
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+#pragma unroll
+                        for (int j = 0; j < 3; ++j)
+                            G[i * 3 + j] = (i == j || i == dir || j == dir)
+                                               ? ring_grad2<T2, WC2, PT, TL, STAGED>(plp, q4, i, j, c, rw, a.sc)
+                                               : Op<T2>::zero();
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) u[i] = cvt<T2>(ldv<PT>(plp[2] + i * PF + q4));
+                    using O = Op<T2>;
+                    const T2 divu = O::add(O::add(G[0], G[4]), G[8]);
+                    T2 acc = O::zero();
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        T2 sij = O::add(G[i * 3 + dir], G[dir * 3 + i]);
+                        if (i == dir) sij = O::sub(sij, O::mul(c.two_thirds, divu));
+                        const T2 tau = O::mul(c.inv_re, sij);
+                        acc = O::add(acc, O::mul(u[i], tau));
+                    }
+                    stv<T>(Lb + 0 * TL::R2N + q2, divu);
+                    stv<T>(Lb + (1 + dir) * TL::R2N + q2, acc);
+                    stv<T>(Lb + (3 + dir) * TL::R2N + q2,
+                           ring_grad2<T2, WC2, PT, TL, STAGED>(plp, q4, 3, dir, c, rw, a.sc));
+                }
+            }
+            if (cpl >= zs - 2 && cpl < ze + 2) nb_arrive(WS_LREADY + (cpl & 1), NALL);
+        }
+        cp_async_wait_all();
+        return;
+    }
+
+    // ========================= consumers ======================================
+    const int ctid = tid - NP;
+    const int tx = ctid % TXP, ty = ctid / TXP;
+    const int x = x0 + 2 * tx, y = y0 + ty;
+    const bool own = x < g.nx && y < g.ny;
+    const long long o = own ? (long long)y * g.nx + x : 0;
+    const int p4 = (ty + 4) * TL::R4X + 2 * tx + 4;
+    const int p2 = (ty + 2) * TL::R2X + 2 * tx + 2;
+
+    T2 wdiv[5], wgz[5], wdt[5];
+    Deferred<T2> dfr[2];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) wdiv[i] = wgz[i] = wdt[i] = Op<T2>::zero();
+
+    for (int cp = zs - 2; cp < ze + 2; ++cp) {
+        // stage-update operands of the late residual (plane cp-2)
+        const bool do_d = cp - 2 >= zs && cp - 2 < ze && own;
+        RkIn2<QS, TS> ind[2];
+        if (do_d) {
+            ind[0] = rk_load2<QS, TS>(a, 3, cp - 2, o);
+            ind[1] = rk_load2<QS, TS>(a, 4, cp - 2, o);
+        }
+        nb_sync(WS_FULL + ((cp + 2) & 1), NALL);  // A(cp+2) done: planes cp-2..cp+2 in the rings
+        const PT* plp[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) plp[i] = Pr + ring_slot(cp - 2 + i) * TL::R4N;
+        T* Lb = Lbuf + (cp & 1) * 5 * TL::R2N;
+        // ---- own part of B(cp) ----
+        if (c.viscous) {
+            T2 G[9], dT[3], u[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int j = 0; j < 3; ++j) G[i * 3 + j] = ring_grad2<T2, WC2, PT, TL, STAGED>(plp, p4, i, j, c, rw, a.sc);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) dT[j] = ring_grad2<T2, WC2, PT, TL, STAGED>(plp, p4, 3, j, c, rw, a.sc);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) u[i] = cvt<T2>(ldv<PT>(plp[2] + i * PF + p4));
+            T2 divu, gg[3];
+            level2_point<T2>(c, G, u, divu, gg);
+            stv<T>(Lb + 0 * TL::R2N + p2, divu);
+            stv<T>(Lb + 1 * TL::R2N + p2, gg[0]);
+            stv<T>(Lb + 2 * TL::R2N + p2, gg[1]);
+            stv<T>(Lb + 3 * TL::R2N + p2, dT[0]);
+            stv<T>(Lb + 4 * TL::R2N + p2, dT[1]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                wdiv[i] = wdiv[i + 1];
+                wgz[i] = wgz[i + 1];
+                wdt[i] = wdt[i + 1];
+            }
+            wdiv[4] = divu;
+            wgz[4] = gg[2];
+            wdt[4] = dT[2];
+        }
+        nb_sync(WS_LREADY + (cp & 1), NALL);  // level-2 of plane cp complete (own + rim)
+        // ---- late residual of plane cp-2 -> RK of rhow, rhoE ----
+        if (do_d) {
+            T2 cw = Op<T2>::zero(), tz = Op<T2>::zero(), hz = Op<T2>::zero();
+            if (c.viscous) {
+                cw = d1v<T2>(wdiv[0], wdiv[1], wdiv[3], wdiv[4], c.r);
+                tz = d1v<T2>(wgz[0], wgz[1], wgz[3], wgz[4], c.r);
+                hz = d1v<T2>(wdt[0], wdt[1], wdt[3], wdt[4], c.r);
+            }
+            T2 rw_, rE;
+            residual_late<T2>(c, dfr[0], cw, tz, hz, rw_, rE);
+            rk_pair<QS, TS, RS, TC, QC, TL>(a, 3, cp - 2, o, cvt<RS2>(rw_), ind[0], x, y);
+            rk_pair<QS, TS, RS, TC, QC, TL>(a, 4, cp - 2, o, cvt<RS2>(rE), ind[1], x, y);
+        }
+        dfr[0] = dfr[1];
+        // ---- early residual of plane cp -> RK of rho, rhou, rhov ----
+        if (cp >= zs && cp < ze && own) {
+            RingAcc2<T2, PT, TL> acc;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                const int s = ring_slot(cp - 2 + i);
+                acc.pp[i] = plp[i] + p4;
+                acc.prs[i] = Ppr + s * TL::R2N + p2;
+                acc.qp[i] = Qr + s * TL::R2N + p2;
+            }
+            acc.lp = Lb + p2;
+            RkIn2<QS, TS> inc[3];
+#pragma unroll
+            for (int comp = 0; comp < 3; ++comp) inc[comp] = rk_load2<QS, TS>(a, comp, cp, o);
+            T2 out[3];
+            residual_early_dirwise<T2, SPL>(c, acc, out, dfr[1]);
+#pragma unroll
+            for (int comp = 0; comp < 3; ++comp)
+                rk_pair<QS, TS, RS, TC, QC, TL>(a, comp, cp, o, cvt<RS2>(out[comp]), inc[comp], x, y);
+        }
+        nb_arrive(WS_EMPTY + ((cp + 4) & 1), NALL);  // planes cp-2.. and level-2 of cp released
+    }
+}
+
+}  // namespace mpfd_b200

@@ -67,3 +67,56 @@ def test_csv_byte_identical(b200, tmp_path, name):
         outs[who] = out.read_bytes()
     assert codes["ref"] == codes["b200"]
     assert outs["ref"] == outs["b200"]
+
+
+def _csv(rows):
+    s = "t,kinetic_energy,enstrophy,solenoidal_dissipation,ke_normalized,diverged\n"
+    for r in rows:
+        s += ",".join("%.17g" % x for x in r) + ",0\n"
+    return s
+
+
+@pytest.mark.skipif(not os.path.exists(REF_CLI), reason="reference CLI not built")
+def test_compare_matches_reference_cli(b200, tmp_path):
+    """`compare a.csv b.csv` (tools/mpfd.cpp:28-38, compare_series tgv.cpp:177-197):
+    same per-sample |delta eps_S|, pairwise mean and max, same text; sample-grid
+    mismatches are errors (exit 1) in both."""
+    tool = build_tool(b200)
+    import numpy as np
+    rng = np.random.default_rng(3)
+    t = np.arange(70) * 0.5
+    a = np.c_[t, rng.random((70, 4))]
+    b = np.c_[t, rng.random((70, 4))]
+    (tmp_path / "a.csv").write_text(_csv(a))
+    (tmp_path / "b.csv").write_text(_csv(b))
+    (tmp_path / "c.csv").write_text(_csv(b[:-1]))
+    (tmp_path / "d.csv").write_text(_csv(np.c_[t + 0.25, b[:, 1:]]))
+    args = [str(tmp_path / "a.csv"), str(tmp_path / "b.csv")]
+    r1 = subprocess.run([REF_CLI, "compare", *args], capture_output=True, text=True)
+    r2 = subprocess.run([tool, "compare", *args], capture_output=True, text=True)
+    assert r1.returncode == r2.returncode == 0
+    assert r1.stdout == r2.stdout
+    for bad in ("c.csv", "d.csv"):
+        args = [str(tmp_path / "a.csv"), str(tmp_path / bad)]
+        assert subprocess.run([REF_CLI, "compare", *args], capture_output=True).returncode == 1
+        assert subprocess.run([tool, "compare", *args], capture_output=True).returncode == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(REF_CLI), reason="reference CLI not built")
+def test_sweep_matrix_identical(b200, tmp_path):
+    """`sweep <spec>` (run_sweep, runner.cpp:108-173): DP reference plus each
+    preset over dt x M; the mean |delta eps_S| matrix (the paper's accuracy
+    heat-map methodology) and the log are the reference CLI's, byte for byte."""
+    tool = build_tool(b200)
+    spec = ("n = 16\nRe = 1600\nt_end = 1.0\nstrategy = storesome\nthreads = 4\n"
+            "sweep.dt = 0.01, 0.02\nsweep.M = 0.1, 0.3\nsweep.presets = SPDP, HPSP, SP\n")
+    outs = {}
+    for who, exe in (("ref", REF_CLI), ("b200", tool)):
+        f = tmp_path / f"{who}.spec"
+        f.write_text(spec + f"sweep.output = {tmp_path / (who + '.csv')}\n")
+        r = subprocess.run([exe, "sweep", str(f)], capture_output=True, text=True, cwd=tmp_path)
+        assert r.returncode == 0, r.stderr
+        outs[who] = (r.stdout.replace(who + ".csv", "X.csv"), (tmp_path / f"{who}.csv").read_bytes())
+    assert outs["ref"] == outs["b200"]
+    assert outs["ref"][1].count(b"\n") == 5

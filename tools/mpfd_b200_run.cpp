@@ -1,11 +1,15 @@
-// mpfd_b200_run -- `mpfd run <config>` (tools/mpfd.cpp:23-26, runner.cpp:69-88)
-// on the B200 path, through the C++ adapter (include/mpfd_b200.hpp).
+// mpfd_b200_run -- the reference CLI's `run`, `compare` and `sweep` commands
+// (tools/mpfd.cpp:23-46; runner.cpp:69-88, 108-173) on the B200 path, through
+// the C++ adapter (include/mpfd_b200.hpp).
 //
 // Reads the reference's `key = value` config (config.cpp:120-235, the keys
 // of the hot path), runs init + advance on cuda:0 and writes the
 // diagnostics CSV in the reference format (io.cpp:19-36, %.17g), so the two
-// CSVs can be compared byte for byte.  Exit codes as the reference CLI:
-// 0 completed, 1 configuration error, 2 diverged.
+// CSVs can be compared byte for byte.  `compare a.csv b.csv` is
+// compare_series (tgv.cpp:177-197) with the reference's output format;
+// `sweep <spec>` is run_sweep: DP reference plus each preset over the dt x M
+// grid, mean |delta eps_S| matrix.  Exit codes as the reference CLI:
+// 0 completed, 1 configuration or comparison error, 2 diverged.
 //
 //   g++ -O2 -std=c++17 -Iinclude tools/mpfd_b200_run.cpp
 //       -Lpaper_2505_20911_b200 -lmpfd_b200 -Wl,-rpath,$PWD/paper_2505_20911_b200
@@ -14,6 +18,9 @@
 #include <fstream>
 #include <iostream>
 #include <map>
+#include <stdexcept>
+#include <vector>
+#include <algorithm>
 #include <sstream>
 #include <string>
 
@@ -35,9 +42,28 @@ struct Cfg {
     long n_iter = -1;
     bool viscous = true;
     std::map<std::string, std::string> custom;  // precision.custom.<name>
+    // sweep spec (config.cpp:259-282)
+    std::vector<double> sweep_dt, sweep_M;
+    std::vector<std::string> sweep_presets;
+    std::string sweep_output;
+    bool saw_t_end = false;
 };
 
-Cfg load(const std::string& path) {
+std::vector<std::string> split_list(const std::string& key, const std::string& v, int ln) {
+    std::vector<std::string> out;
+    std::string item;
+    std::istringstream in(v);
+    while (std::getline(in, item, ',')) {
+        item = trim(item);
+        if (!item.empty()) out.push_back(item);
+    }
+    if (out.empty())
+        throw mpfd_b200::ConfigError("line " + std::to_string(ln) + ": field '" + key +
+                                     "' expects a comma-separated list");
+    return out;
+}
+
+Cfg load(const std::string& path, bool sweep = false) {
     std::ifstream in(path);
     if (!in) throw mpfd_b200::ConfigError("cannot open config file: " + path);
     Cfg c;
@@ -73,8 +99,17 @@ Cfg load(const std::string& path) {
         else if (k == "output") c.output = v;
         else if (k == "threads") c.threads = std::stoi(v);
         else if (k.rfind("precision.custom.", 0) == 0) c.custom[k.substr(17)] = v;
+        else if (sweep && k == "sweep.dt") { for (auto& x : split_list(k, v, ln)) c.sweep_dt.push_back(std::stod(x)); }
+        else if (sweep && k == "sweep.M") { for (auto& x : split_list(k, v, ln)) c.sweep_M.push_back(std::stod(x)); }
+        else if (sweep && k == "sweep.presets") {
+            c.sweep_presets = split_list(k, v, ln);
+            for (const auto& pr : c.sweep_presets) mpfd_b200::resolve_preset(pr.c_str());  // validate
+        }
+        else if (sweep && k == "sweep.output") c.sweep_output = v;
         else throw mpfd_b200::ConfigError("line " + std::to_string(ln) + ": unknown key '" + k + "'");
     }
+    if (sweep && c.sweep_presets.empty()) throw mpfd_b200::ConfigError("sweep spec: missing 'sweep.presets'");
+    c.saw_t_end = saw_t;
     // finalize_sim (config.cpp:217-235)
     if (c.n_iter >= 0 && !saw_t) c.t_end = c.n_iter * c.dt;
     if (c.n_iter < 0) c.n_iter = std::lround(c.t_end / c.dt);
@@ -88,65 +123,215 @@ void g17(std::string& out, double v) {
     out += b;
 }
 
+struct Run {
+    std::vector<mpfd_diag> series;
+    bool diverged = false;
+    mpfd_b200::AdvanceResult raw;
+};
+
+// run_simulation (runner.cpp:11-48) on cuda:0
+Run run_cfg(const Cfg& c) {
+    mpfd_precision p = mpfd_b200::resolve_preset(c.precision.c_str());
+    p.emulation = c.emulation == "storeround" ? MPFD_STOREROUND : MPFD_STRICT;
+    std::vector<std::string> names;
+    std::vector<const char*> np;
+    std::vector<int> kinds;
+    for (const auto& kv : c.custom) {
+        names.push_back(kv.first);
+        kinds.push_back(kv.second == "B16" ? MPFD_B16 : kv.second == "B32" ? MPFD_B32 : MPFD_B64);
+    }
+    for (const auto& s : names) np.push_back(s.c_str());
+    p.n_overrides = (int)names.size();
+    p.override_names = np.data();
+    p.override_kinds = kinds.data();
+    const mpfd_flow flow{c.M, c.Re, c.Pr, c.gamma, c.viscous ? 1 : 0};
+    mpfd_b200::Solver s(c.n, p, c.strategy == "storesome" ? MPFD_STORESOME : MPFD_DEFAULT, flow,
+                        mpfd_b200::split_preset(c.split.c_str()));
+    if (c.case_kind == "tgv") s.init_tgv();
+    else s.init_uniform();
+    mpfd_step st = mpfd_b200::default_step(c.dt, c.n_iter, c.diag_interval);
+    st.ke_weighting = c.ke == "density" ? MPFD_KE_DENSITY : MPFD_KE_PLAIN;
+    st.threads = c.threads;
+    Run r;
+    r.raw = s.advance(st);
+    r.series = r.raw.series;
+    r.diverged = r.raw.diverged;
+    return r;
+}
+
+int cmd_run(const char* path) {
+    const Cfg c = load(path);
+    const Run run = run_cfg(c);
+    const auto& r = run.raw;
+    std::string csv = "t,kinetic_energy,enstrophy,solenoidal_dissipation,ke_normalized,diverged\n";
+    for (const auto& d : r.series) {
+        g17(csv, d.t);
+        csv += ',';
+        g17(csv, d.kinetic_energy);
+        csv += ',';
+        g17(csv, d.enstrophy);
+        csv += ',';
+        g17(csv, d.eps_s);
+        csv += ',';
+        g17(csv, d.ke_normalized);
+        csv += d.diverged ? ",1\n" : ",0\n";
+    }
+    std::ofstream(c.output, std::ios::binary) << csv;
+    std::cout << "wrote " << c.output << " (" << r.series.size() << " samples)\n";
+    if (r.diverged) {
+        const auto& e = *r.divergence;
+        std::cout << "DIVERGED at t = " << e.time << " (iteration " << e.iteration << ", substep "
+                  << e.substep << "): " << e.what << " first at (" << e.i << "," << e.j << "," << e.k
+                  << ")\n";
+        return 2;
+    }
+    return 0;
+}
+
+// read_diagnostics_csv (io.cpp:46-67)
+struct Rec {
+    double t, ke, ens, eps, ken;
+    int div;
+};
+std::vector<Rec> read_csv(const std::string& path) {
+    std::ifstream f(path);
+    if (!f) throw std::runtime_error("cannot open: " + path);
+    std::string line;
+    if (!std::getline(f, line)) throw std::runtime_error("empty CSV: " + path);
+    if (line.rfind("t,kinetic_energy", 0) != 0) throw std::runtime_error("unexpected CSV header in " + path);
+    std::vector<Rec> out;
+    int ln = 1;
+    while (std::getline(f, line)) {
+        ++ln;
+        if (line.empty()) continue;
+        Rec r;
+        if (std::sscanf(line.c_str(), "%lf,%lf,%lf,%lf,%lf,%d", &r.t, &r.ke, &r.ens, &r.eps, &r.ken, &r.div) != 6)
+            throw std::runtime_error(path + ": malformed CSV row at line " + std::to_string(ln));
+        out.push_back(r);
+    }
+    return out;
+}
+
+// pairwise_sum (reduce.cpp:14-22), leaf 32
+double pairwise_sum(const double* v, size_t n) {
+    if (n <= 32) {
+        double s = 0.0;
+        for (size_t i = 0; i < n; ++i) s += v[i];
+        return s;
+    }
+    const size_t h = n / 2;
+    return pairwise_sum(v, h) + pairwise_sum(v + h, n - h);
+}
+
+// compare_series (tgv.cpp:177-197): candidate vs reference eps_S
+struct Cmp {
+    std::vector<double> t, d;
+    double mean = 0.0, max = 0.0;
+};
+Cmp compare(const std::vector<double>& ta, const std::vector<double>& ea, const std::vector<double>& tb,
+            const std::vector<double>& eb) {
+    if (ta.size() != tb.size())
+        throw std::runtime_error("sample counts differ (" + std::to_string(ta.size()) + " vs " +
+                                 std::to_string(tb.size()) + ")");
+    Cmp c;
+    for (size_t i = 0; i < ta.size(); ++i) {
+        if (ta[i] != tb[i]) throw std::runtime_error("sample grids differ at index " + std::to_string(i));
+        c.t.push_back(ta[i]);
+        c.d.push_back(std::abs(ea[i] - eb[i]));
+    }
+    if (!c.d.empty()) {
+        c.mean = pairwise_sum(c.d.data(), c.d.size()) / (double)c.d.size();
+        for (double x : c.d) c.max = std::max(c.max, x);
+    }
+    return c;
+}
+
+int cmd_compare(const char* a, const char* b) {
+    const auto A = read_csv(a), B = read_csv(b);
+    std::vector<double> ta, ea, tb, eb;
+    for (const auto& r : A) ta.push_back(r.t), ea.push_back(r.eps);
+    for (const auto& r : B) tb.push_back(r.t), eb.push_back(r.eps);
+    const Cmp c = compare(ta, ea, tb, eb);
+    std::printf("t,abs_diff_eps_s\n");
+    for (size_t i = 0; i < c.t.size(); ++i) std::printf("%.17g,%.17g\n", c.t[i], c.d[i]);
+    std::printf("mean_abs_diff=%.17g\n", c.mean);
+    std::printf("max_abs_diff=%.17g\n", c.max);
+    return 0;
+}
+
+// run_sweep (runner.cpp:108-173)
+int cmd_sweep(const char* path) {
+    const Cfg spec = load(path, true);
+    const std::vector<double> dts = spec.sweep_dt.empty() ? std::vector<double>{spec.dt} : spec.sweep_dt;
+    const std::vector<double> machs = spec.sweep_M.empty() ? std::vector<double>{spec.M} : spec.sweep_M;
+    std::string csv = "dt,M";
+    for (const auto& p : spec.sweep_presets) csv += "," + p;
+    csv += "\n";
+    for (double dt : dts) {
+        for (double mach : machs) {
+            Cfg cell = spec;
+            cell.dt = dt;
+            cell.M = mach;
+            cell.n_iter = std::lround(cell.t_end / dt);
+            cell.diag_interval = (int)std::max(1l, std::lround(0.5 / dt));
+            Cfg ref = cell;
+            ref.precision = "DP";
+            ref.custom.clear();
+            std::cout << "sweep: DP reference at dt=" << dt << " M=" << mach << "\n";
+            const Run rr = run_cfg(ref);
+            char num[32];
+            std::snprintf(num, sizeof num, "%.17g", dt);
+            csv += num;
+            std::snprintf(num, sizeof num, ",%.17g", mach);
+            csv += num;
+            for (const auto& preset : spec.sweep_presets) {
+                Cfg cand = cell;
+                cand.precision = preset;
+                cand.custom.clear();
+                std::cout << "sweep: " << preset << " at dt=" << dt << " M=" << mach << "\n";
+                const Run cr = run_cfg(cand);
+                if (cr.diverged || rr.diverged) {
+                    csv += ",inf";
+                    continue;
+                }
+                std::vector<double> ta, ea, tb, eb;
+                for (const auto& d : cr.series) ta.push_back(d.t), ea.push_back(d.eps_s);
+                for (const auto& d : rr.series) tb.push_back(d.t), eb.push_back(d.eps_s);
+                std::snprintf(num, sizeof num, ",%.17g", compare(ta, ea, tb, eb).mean);
+                csv += num;
+            }
+            csv += "\n";
+        }
+    }
+    if (!spec.sweep_output.empty()) {
+        std::ofstream f(spec.sweep_output, std::ios::binary);
+        if (!f) throw std::runtime_error("cannot open for writing: " + spec.sweep_output);
+        f << csv;
+    }
+    std::cout << csv;
+    if (!spec.sweep_output.empty()) std::cout << "wrote " << spec.sweep_output << "\n";
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
-    if (argc != 3 || std::string(argv[1]) != "run") {
-        std::cerr << "usage: mpfd_b200_run run <config>\n";
-        return 1;
-    }
+    const std::string cmd = argc > 1 ? argv[1] : "";
     try {
-        const Cfg c = load(argv[2]);
-        mpfd_precision p = mpfd_b200::resolve_preset(c.precision.c_str());
-        p.emulation = c.emulation == "storeround" ? MPFD_STOREROUND : MPFD_STRICT;
-        std::vector<std::string> names;
-        std::vector<const char*> np;
-        std::vector<int> kinds;
-        for (const auto& kv : c.custom) {
-            names.push_back(kv.first);
-            kinds.push_back(kv.second == "B16" ? MPFD_B16 : kv.second == "B32" ? MPFD_B32 : MPFD_B64);
-        }
-        for (const auto& s : names) np.push_back(s.c_str());
-        p.n_overrides = (int)names.size();
-        p.override_names = np.data();
-        p.override_kinds = kinds.data();
-        const mpfd_flow flow{c.M, c.Re, c.Pr, c.gamma, c.viscous ? 1 : 0};
-        mpfd_b200::Solver s(c.n, p, c.strategy == "storesome" ? MPFD_STORESOME : MPFD_DEFAULT, flow,
-                            mpfd_b200::split_preset(c.split.c_str()));
-        if (c.case_kind == "tgv") s.init_tgv();
-        else s.init_uniform();
-        mpfd_step st = mpfd_b200::default_step(c.dt, c.n_iter, c.diag_interval);
-        st.ke_weighting = c.ke == "density" ? MPFD_KE_DENSITY : MPFD_KE_PLAIN;
-        st.threads = c.threads;
-        const auto r = s.advance(st);
-        std::string csv = "t,kinetic_energy,enstrophy,solenoidal_dissipation,ke_normalized,diverged\n";
-        for (const auto& d : r.series) {
-            g17(csv, d.t);
-            csv += ',';
-            g17(csv, d.kinetic_energy);
-            csv += ',';
-            g17(csv, d.enstrophy);
-            csv += ',';
-            g17(csv, d.eps_s);
-            csv += ',';
-            g17(csv, d.ke_normalized);
-            csv += d.diverged ? ",1\n" : ",0\n";
-        }
-        std::ofstream(c.output, std::ios::binary) << csv;
-        std::cout << "wrote " << c.output << " (" << r.series.size() << " samples)\n";
-        if (r.diverged) {
-            const auto& e = *r.divergence;
-            std::cout << "DIVERGED at t = " << e.time << " (iteration " << e.iteration << ", substep "
-                      << e.substep << "): " << e.what << " first at (" << e.i << "," << e.j << "," << e.k
-                      << ")\n";
-            return 2;
-        }
-        return 0;
+        if (cmd == "run" && argc == 3) return cmd_run(argv[2]);
+        if (cmd == "compare" && argc == 4) return cmd_compare(argv[2], argv[3]);
+        if (cmd == "sweep" && argc == 3) return cmd_sweep(argv[2]);
+        std::cerr << "usage:\n  mpfd_b200_run run <config>\n  mpfd_b200_run compare <a.csv> <b.csv>\n"
+                     "  mpfd_b200_run sweep <spec>\n";
+        return 1;
     } catch (const mpfd_b200::ConfigError& e) {
         std::cerr << "error: " << e.what() << "\n";
         return 1;
-    } catch (const std::exception& e) {
+    } catch (const mpfd_b200::DeviceError& e) {
         std::cerr << "error: " << e.what() << "\n";
         return 3;
+    } catch (const std::exception& e) {
+        std::cerr << "error: " << e.what() << "\n";
+        return 1;
     }
 }
