@@ -7,6 +7,8 @@
 // from the two aligned neighbouring pairs.
 #pragma once
 
+#include <stdexcept>
+
 #include "kernels_fused.cuh"
 
 namespace mpfd_b200 {
@@ -542,13 +544,26 @@ struct FusedPlan {
     }
 
 #ifndef MPFD_WS
-#define MPFD_WS 0
+#define MPFD_WS 1
 #endif
     // warp-specialised kernel (kernels_ws.cuh): fp16 64x12 tile with 4
     // producer warps, fp32 32x12 with 2
-    using TLW = typename std::conditional<sizeof(T) == 2, TileWS<64, 12>, TileWS<32, 12>>::type;
-    static constexpr int NPW = sizeof(T) == 2 ? 4 : 2;
-    static constexpr bool WS = MPFD_WS != 0 && PAIR && WsSmem<TLW, T, PT, QS>::total <= 232448;
+#ifndef MPFD_WS_TY
+#define MPFD_WS_TY 12
+#endif
+#ifndef MPFD_WS_NPW
+#define MPFD_WS_NPW 8
+#endif
+#ifndef MPFD_WS32
+#define MPFD_WS32 0
+#endif
+#ifndef MPFD_WS32_NPW
+#define MPFD_WS32_NPW 4
+#endif
+    using TLW = typename std::conditional<sizeof(T) == 2, TileWS<64, MPFD_WS_TY>, TileWS<32, 12>>::type;
+    static constexpr int NPW = sizeof(T) == 2 ? MPFD_WS_NPW : MPFD_WS32_NPW;
+    static constexpr bool WS = MPFD_WS != 0 && PAIR && (sizeof(T) == 2 || MPFD_WS32 != 0) &&
+                               WsSmem<TLW, T, PT, QS>::total <= 232448;
 
     template <bool ST, unsigned SPL>
     static void go(FusedArgs a, cudaStream_t st) {
@@ -556,11 +571,13 @@ struct FusedPlan {
             if (a.g.nx % 2 == 0) {
                 auto kern = k_fused_ws<QS, TS, RS, PT, WC, T, TC, QC, ST, TLW, NPW, SPL>;
                 constexpr size_t smem = WsSmem<TLW, T, PT, QS>::total;
-                static bool attr = false;
-                if (!attr) {
+                static int ok = -1;
+                if (ok < 0) {
                     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                    attr = true;
+                    cudaFuncAttributes fa{};
+                    ok = cudaFuncGetAttributes(&fa, kern) == cudaSuccess && WsRegs<T, TLW, NPW>::fits(fa.numRegs);
                 }
+                if (!ok) throw std::runtime_error("warp-specialised kernel: register split exceeds the launch pool");
                 a.lz = z_range(a.g, a.zhi - a.zlo, TLW::TX, TLW::TY, 1);
                 const dim3 grid((a.g.nx + TLW::TX - 1) / TLW::TX, (a.g.ny + TLW::TY - 1) / TLW::TY,
                                 (a.zhi - a.zlo + a.lz - 1) / a.lz);

@@ -56,9 +56,36 @@ __device__ __forceinline__ void nb_arrive(int id, int n) {
     __threadfence_block();
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-enum WsBar { WS_PROD = 1, WS_FULL = 2, WS_LREADY = 4, WS_EMPTY = 6 };  // +0/+1 by plane parity
+enum WsBar { WS_PROD = 1, WS_FULL = 2, WS_LREADY = 4, WS_EMPTY = 6, WS_FULLC = 8 };  // +0/+1 by plane parity
+
+#ifndef MPFD_WS_OWNA
+#define MPFD_WS_OWNA 0
+#endif
 
 __device__ __forceinline__ int ring_slot(int p) { return (p + 12) % 6; }
+
+#ifndef MPFD_WS_PREG
+#define MPFD_WS_PREG 56
+#endif
+#ifndef MPFD_WS32_PREG
+#define MPFD_WS32_PREG 0
+#endif
+// register split between the roles: producer warpgroups shrink to PREG
+// registers per thread (setmaxnreg.dec) and consumers grow to CREG
+// (setmaxnreg.inc) within the CTA's launch pool of `launch_regs` per thread.
+// The host checks the split against the kernel's actual register count
+// before the first launch (an over-subscribed .inc would wait forever).
+template <class T, class TL, int NPW>
+struct WsRegs {
+    static constexpr int NP = NPW * 32, NC = TL::NT / 2, NALL = NP + NC;
+    static constexpr int PREG = (NPW % 4 == 0) ? (sizeof(T) == 2 ? MPFD_WS_PREG : MPFD_WS32_PREG) : 0;
+    static constexpr int LAUNCH = 65536 / NALL / 8 * 8;
+    static constexpr int CREG0 = PREG > 0 ? (LAUNCH * NALL - PREG * NP) / NC / 8 * 8 : 0;
+    static constexpr int CREG = CREG0 > 256 ? 256 : CREG0;
+    static bool fits(int launch_regs) {
+        return PREG == 0 || (long)PREG * NP + (long)CREG * NC <= (long)launch_regs * NALL;
+    }
+};
 
 template <class QS, class TS, class RS, class PT, class WC, class T, class TC, class QC, bool STAGED, class TL,
           int NPW, unsigned SPL>
@@ -94,108 +121,140 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
     const WC2 rw = kget<WC2>(a.kb[K_R_STAGE]);
     const QS* qin = (const QS*)a.qin;
     constexpr int PF = TL::NRING * TL::R4N;
+    // OWNA: consumers compute phase A at their own pair (the tile interior);
+    // producers only on the 4-point ring around it
+    constexpr bool OWNA = MPFD_WS_OWNA != 0;
+    const WC2 half = kget<WC2>(a.kb[K_HALF]), gm1 = kget<WC2>(a.kb[K_GM1]), gM2 = kget<WC2>(a.kb[K_GM2]);
 
+    // phase A of one point pair: staging pair index si, rim descriptor ri
+    // (element index | R2 index << 13 | in R2 << 26 | owned interior << 27),
+    // wrapped in-plane offset roff; copies plane p+1 into its staging entries
+    auto a_pair = [&](int p, int si, unsigned ri, int roff) {
+        const int slot = ring_slot(p);
+        const QS* sp = Sg + 2 * si;
+        const QS2 q0 = ldv<QS>(sp), q1 = ldv<QS>(sp + TL::R4N), q2 = ldv<QS>(sp + 2 * TL::R4N),
+                  q3 = ldv<QS>(sp + 3 * TL::R4N), q4 = ldv<QS>(sp + 4 * TL::R4N);
+        const WC2 rho = cvt<WC2>(q0);
+        const PrimOut<WC2> pv =
+            PrimCalc<WC2>::run(rho, cvt<WC2>(q1), cvt<WC2>(q2), cvt<WC2>(q3), cvt<WC2>(q4), half, gm1, gM2);
+        if (p + 1 < ze + 4) {
+            // this thread's staging entries were consumed (their loads fed the
+            // primitives above): copy plane p+1 into them
+            const QS* qb = qin + (long long)(p + 1 + kHalo) * 5 * g.plane + roff;
+#pragma unroll
+            for (int cc = 0; cc < 5; ++cc) cp_async<2 * sizeof(QS)>(Sg + cc * TL::R4N + 2 * si, qb + cc * g.plane);
+        }
+        const int rnd = SPL != 0 ? 0 : a.pc.round;
+        PT* pp = Pr + slot * TL::R4N + (ri & 0x1FFFu);
+        stv<PT>(pp, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[0], pv.ux)));
+        stv<PT>(pp + PF, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[1], pv.uy)));
+        stv<PT>(pp + 2 * PF, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[2], pv.uz)));
+        stv<PT>(pp + 3 * PF, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[4], pv.Tv)));
+        if (ri & (1u << 26)) {
+            const int q2i = (int)((ri >> 13) & 0x1FFFu);
+            stv<PT>(Ppr + slot * TL::R2N + q2i, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[3], pv.pr)));
+            T* qq = Qr + slot * TL::R2N + q2i;
+            constexpr int QF = TL::NRING * TL::R2N;
+            stv<T>(qq, cvt<T2>(q0));
+            stv<T>(qq + QF, cvt<T2>(q1));
+            stv<T>(qq + 2 * QF, cvt<T2>(q2));
+            stv<T>(qq + 3 * QF, cvt<T2>(q3));
+            stv<T>(qq + 4 * QF, cvt<T2>(q4));
+        }
+        if ((ri & (1u << 27)) && p >= zs && p < ze) {
+            using OS = Op<WC>;
+            const bool b0 = !OS::positive(lo(rho)) || nonfinite(lo(rho));
+            const bool b1 = !OS::positive(hi(rho)) || nonfinite(hi(rho));
+            if (b0 | b1)
+                report_rho<TL>(g, a.div, a.iter, a.sub, p, (int)(ri & 0x1FFFu), (b0 ? 1u : 0u) | (b1 ? 2u : 0u));
+        }
+    };
+    auto wrap_off = [&](int rx, int ry) {
+        int xx = x0 - 4 + rx, yy = y0 - 4 + ry;
+        xx %= g.nx;
+        if (xx < 0) xx += g.nx;
+        yy %= g.ny;
+        if (yy < 0) yy += g.ny;
+        return yy * g.nx + xx;
+    };
+    auto rim_desc = [&](int rx, int ry) {
+        const bool in2 = rx >= 2 && rx < TL::TX + 6 && ry >= 2 && ry < TL::TY + 6;
+        const bool inner = rx >= 4 && rx < TL::TX + 4 && ry >= 4 && ry < TL::TY + 4 && x0 - 4 + rx < g.nx &&
+                           y0 - 4 + ry < g.ny;
+        return (unsigned)(ry * TL::R4X + rx) | ((unsigned)(in2 ? (ry - 2) * TL::R2X + (rx - 2) : 0) << 13) |
+               (in2 ? 1u << 26 : 0u) | (inner ? 1u << 27 : 0u);
+    };
+
+    // producer warpgroups give registers to the consumers (WsRegs)
+    constexpr int PREG = WsRegs<T, TL, NPW>::PREG;
+    constexpr int CREG = WsRegs<T, TL, NPW>::CREG;
+    static_assert(PREG == 0 || (NPW % 4 == 0 && CREG >= 24), "register split");
     if (tid < NP) {
         // ======================= producers ====================================
+        if constexpr (PREG > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PREG));
         const int ptid = tid;
-        const WC2 half = kget<WC2>(a.kb[K_HALF]), gm1 = kget<WC2>(a.kb[K_GM1]), gM2 = kget<WC2>(a.kb[K_GM2]);
-        constexpr int KPF = (R4NP + NP - 1) / NP;
-        int rim_off[KPF];
+        // this producer's rim pairs: the whole R4 box, or (OWNA) the ring of
+        // pairs around the tile interior
+        constexpr int NRIM = OWNA ? 8 * R4P + 4 * TL::TY : R4NP;
+        constexpr int KPF = (NRIM + NP - 1) / NP;
+        int rim_off[KPF], rsi[KPF];
         unsigned rinfo[KPF];
-        const bool fastwrap = g.nx >= TL::TX + 8 && g.ny >= TL::TY + 8;
 #pragma unroll
         for (int k = 0; k < KPF; ++k) {
-            const int i = min(ptid + k * NP, R4NP - 1);
-            const int ry = i / R4P, rx = 2 * (i - ry * R4P);
-            int xx = x0 - 4 + rx, yy = y0 - 4 + ry;
-            if (fastwrap) {
-                xx += xx < 0 ? g.nx : 0;
-                xx -= xx >= g.nx ? g.nx : 0;
-                yy += yy < 0 ? g.ny : 0;
-                yy -= yy >= g.ny ? g.ny : 0;
+            const int j = min(ptid + k * NP, NRIM - 1);
+            int ry, pc;
+            if (!OWNA) {
+                ry = j / R4P;
+                pc = j - ry * R4P;
+            } else if (j < 4 * R4P) {
+                ry = j / R4P;
+                pc = j - ry * R4P;
+            } else if (j < 4 * R4P + 4 * TL::TY) {
+                const int kk = j - 4 * R4P, cc = kk & 3;
+                ry = 4 + (kk >> 2);
+                pc = cc < 2 ? cc : TXP + cc;
             } else {
-                xx %= g.nx;
-                if (xx < 0) xx += g.nx;
-                yy %= g.ny;
-                if (yy < 0) yy += g.ny;
+                const int kk = j - 4 * R4P - 4 * TL::TY;
+                ry = TL::TY + 4 + kk / R4P;
+                pc = kk - (kk / R4P) * R4P;
             }
-            rim_off[k] = yy * g.nx + xx;
-            const bool in2 = rx >= 2 && rx < TL::TX + 6 && ry >= 2 && ry < TL::TY + 6;
-            const bool inner = rx >= 4 && rx < TL::TX + 4 && ry >= 4 && ry < TL::TY + 4 && x0 - 4 + rx < g.nx &&
-                               y0 - 4 + ry < g.ny;
-            rinfo[k] = (unsigned)(ry * TL::R4X + rx) | ((unsigned)(in2 ? (ry - 2) * TL::R2X + (rx - 2) : 0) << 13) |
-                       (in2 ? 1u << 26 : 0u) | (inner ? 1u << 27 : 0u);
+            rsi[k] = ry * R4P + pc;
+            rim_off[k] = wrap_off(2 * pc, ry);
+            rinfo[k] = rim_desc(2 * pc, ry);
         }
         // each producer thread copies exactly the staging entries it reads
-        auto stage_issue = [&](int p) {
-            const QS* qb = qin + (long long)(p + kHalo) * 5 * g.plane;
+        {
+            const QS* qb = qin + (long long)(zs - 4 + kHalo) * 5 * g.plane;
 #pragma unroll
             for (int k = 0; k < KPF; ++k) {
-                const int i = ptid + k * NP;
-                if (i >= R4NP) break;
+                if (ptid + k * NP >= NRIM) break;
 #pragma unroll
                 for (int cc = 0; cc < 5; ++cc)
-                    cp_async<2 * sizeof(QS)>(Sg + cc * TL::R4N + 2 * i, qb + cc * g.plane + rim_off[k]);
+                    cp_async<2 * sizeof(QS)>(Sg + cc * TL::R4N + 2 * rsi[k], qb + cc * g.plane + rim_off[k]);
             }
             cp_async_commit();
-        };
-        stage_issue(zs - 4);
+        }
 
         for (int p = zs - 4; p < ze + 4; ++p) {
             // A(p) overwrites the slot of plane p-6 (last read by C(p-4)); the
             // rim part of B(p-2) below overwrites the level-2 buffer of p-4
             if (p >= zs + 2) nb_sync(WS_EMPTY + (p & 1), NALL);
             cp_async_wait_all();
-            const int slot = ring_slot(p);
 #pragma unroll
             for (int k = 0; k < KPF; ++k) {
-                const int i = ptid + k * NP;
-                if (i >= R4NP) break;
-                const unsigned ri = rinfo[k];
-                const QS* sp = Sg + 2 * i;
-                const QS2 q0 = ldv<QS>(sp), q1 = ldv<QS>(sp + TL::R4N), q2 = ldv<QS>(sp + 2 * TL::R4N),
-                          q3 = ldv<QS>(sp + 3 * TL::R4N), q4 = ldv<QS>(sp + 4 * TL::R4N);
-                const WC2 rho = cvt<WC2>(q0);
-                const PrimOut<WC2> pv =
-                    PrimCalc<WC2>::run(rho, cvt<WC2>(q1), cvt<WC2>(q2), cvt<WC2>(q3), cvt<WC2>(q4), half, gm1, gM2);
-                if (p + 1 < ze + 4) {
-                    // this thread's staging entries were consumed (their loads
-                    // fed the primitives above): copy plane p+1 into them
-                    const QS* qb = qin + (long long)(p + 1 + kHalo) * 5 * g.plane + rim_off[k];
-#pragma unroll
-                    for (int cc = 0; cc < 5; ++cc) cp_async<2 * sizeof(QS)>(Sg + cc * TL::R4N + 2 * i, qb + cc * g.plane);
-                }
-                const int rnd = SPL != 0 ? 0 : a.pc.round;
-                PT* pp = Pr + slot * TL::R4N + (ri & 0x1FFFu);
-                stv<PT>(pp, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[0], pv.ux)));
-                stv<PT>(pp + PF, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[1], pv.uy)));
-                stv<PT>(pp + 2 * PF, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[2], pv.uz)));
-                stv<PT>(pp + 3 * PF, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[4], pv.Tv)));
-                if (ri & (1u << 26)) {
-                    const int q2i = (int)((ri >> 13) & 0x1FFFu);
-                    stv<PT>(Ppr + slot * TL::R2N + q2i, cvt<PT2>(RKV<WC2>(rnd, a.pc.kind[3], pv.pr)));
-                    T* qq = Qr + slot * TL::R2N + q2i;
-                    constexpr int QF = TL::NRING * TL::R2N;
-                    stv<T>(qq, cvt<T2>(q0));
-                    stv<T>(qq + QF, cvt<T2>(q1));
-                    stv<T>(qq + 2 * QF, cvt<T2>(q2));
-                    stv<T>(qq + 3 * QF, cvt<T2>(q3));
-                    stv<T>(qq + 4 * QF, cvt<T2>(q4));
-                }
-                if ((ri & (1u << 27)) && p >= zs && p < ze) {
-                    using OS = Op<WC>;
-                    const bool b0 = !OS::positive(lo(rho)) || nonfinite(lo(rho));
-                    const bool b1 = !OS::positive(hi(rho)) || nonfinite(hi(rho));
-                    if (b0 | b1) report_rho<TL>(g, a.div, a.iter, a.sub, p, (int)(ri & 0x1FFFu),
-                                                (b0 ? 1u : 0u) | (b1 ? 2u : 0u));
-                }
+                if (ptid + k * NP >= NRIM) break;
+                a_pair(p, rsi[k], rinfo[k], rim_off[k]);
             }
             cp_async_commit();
             if (p >= zs) nb_arrive(WS_FULL + (p & 1), NALL);
             // ---- rim part of B(p-2): needs A(p) of every producer ----
             const int cpl = p - 2;
+            // A(p) complete everywhere: producers (and, OWNA, consumers' own pairs)
+            if (cpl >= zs - 2 && cpl < ze + 2) {
+                if (OWNA) nb_sync(WS_FULLC + (p & 1), NALL);
+                else if (c.viscous) nb_sync(WS_PROD, NP);
+            }
             if (c.viscous && cpl >= zs - 2 && cpl < ze + 2) {
-                nb_sync(WS_PROD, NP);
                 const PT* plp[5];
 #pragma unroll
                 for (int i = 0; i < 5; ++i) plp[i] = Pr + ring_slot(cpl - 2 + i) * TL::R4N;
@@ -250,6 +309,7 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
     }
 
     // ========================= consumers ======================================
+    if constexpr (PREG > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CREG));
     const int ctid = tid - NP;
     const int tx = ctid % TXP, ty = ctid / TXP;
     const int x = x0 + 2 * tx, y = y0 + ty;
@@ -262,6 +322,23 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
     Deferred<T2> dfr[2];
 #pragma unroll
     for (int i = 0; i < 5; ++i) wdiv[i] = wgz[i] = wdt[i] = Op<T2>::zero();
+
+    // OWNA: phase A at this thread's own pair (tile interior)
+    const int own_si = (ty + 4) * R4P + tx + 2;
+    const unsigned own_ri = rim_desc(2 * tx + 4, ty + 4);
+    const int own_off = wrap_off(2 * tx + 4, ty + 4);
+    if constexpr (OWNA) {
+        const QS* qb = qin + (long long)(zs - 4 + kHalo) * 5 * g.plane + own_off;
+#pragma unroll
+        for (int cc = 0; cc < 5; ++cc) cp_async<2 * sizeof(QS)>(Sg + cc * TL::R4N + 2 * own_si, qb + cc * g.plane);
+        cp_async_commit();
+        for (int p = zs - 4; p <= zs; ++p) {
+            cp_async_wait_all();
+            a_pair(p, own_si, own_ri, own_off);
+            cp_async_commit();
+        }
+        nb_arrive(WS_FULLC + (zs & 1), NALL);
+    }
 
     for (int cp = zs - 2; cp < ze + 2; ++cp) {
         // stage-update operands of the late residual (plane cp-2)
@@ -339,8 +416,19 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
             for (int comp = 0; comp < 3; ++comp)
                 rk_pair<QS, TS, RS, TC, QC, TL>(a, comp, cp, o, cvt<RS2>(out[comp]), inc[comp], x, y);
         }
+        if constexpr (OWNA) {
+            // plane cp+3 at the own pair: its slot (plane cp-3) was last read
+            // by C(cp-1) and B(cp-1), both complete (LREADY(cp) above)
+            if (cp + 3 < ze + 4) {
+                cp_async_wait_all();
+                a_pair(cp + 3, own_si, own_ri, own_off);
+                cp_async_commit();
+                nb_arrive(WS_FULLC + ((cp + 3) & 1), NALL);
+            }
+        }
         nb_arrive(WS_EMPTY + ((cp + 4) & 1), NALL);  // planes cp-2.. and level-2 of cp released
     }
+    cp_async_wait_all();
 }
 
 }  // namespace mpfd_b200
