@@ -78,7 +78,10 @@ __device__ __forceinline__ int ring_slot(int p) { return (p + 12) % 6; }
 template <class T, class TL, int NPW>
 struct WsRegs {
     static constexpr int NP = NPW * 32, NC = TL::NT / 2, NALL = NP + NC;
-    static constexpr int PREG = (NPW % 4 == 0) ? (sizeof(T) == 2 ? MPFD_WS_PREG : MPFD_WS32_PREG) : 0;
+    // setmaxnreg is warpgroup-wide (.sync.aligned): both roles must be whole
+    // warpgroups, else a partial warpgroup would wait forever
+    static constexpr int PREG =
+        (NPW % 4 == 0 && (TL::NT / 2) % 128 == 0) ? (sizeof(T) == 2 ? MPFD_WS_PREG : MPFD_WS32_PREG) : 0;
     static constexpr int LAUNCH = 65536 / NALL / 8 * 8;
     static constexpr int CREG0 = PREG > 0 ? (LAUNCH * NALL - PREG * NP) / NC / 8 * 8 : 0;
     static constexpr int CREG = CREG0 > 256 ? 256 : CREG0;
