@@ -563,7 +563,11 @@ struct FusedPlan {
 #ifndef MPFD_WS32_TY
 #define MPFD_WS32_TY 8
 #endif
-    using TLW = typename std::conditional<sizeof(T) == 2, TileWS<64, MPFD_WS_TY>, TileWS<32, MPFD_WS32_TY>>::type;
+#ifndef MPFD_WS_NR
+#define MPFD_WS_NR 6
+#endif
+    using TLW = typename std::conditional<sizeof(T) == 2, TileWS<64, MPFD_WS_TY, MPFD_WS_NR>,
+                                          TileWS<32, MPFD_WS32_TY>>::type;
     static constexpr int NPW = sizeof(T) == 2 ? MPFD_WS_NPW : MPFD_WS32_NPW;
     static constexpr bool WS = MPFD_WS != 0 && PAIR && (sizeof(T) == 2 || MPFD_WS32 != 0) &&
                                WsSmem<TLW, T, PT, QS>::total <= 232448;

@@ -31,12 +31,21 @@
 
 namespace mpfd_b200 {
 
-template <int TX_, int TY_>
+// NR ring slots (>= 6): A(p) may run NR-6 planes further ahead of the
+// residual; the level-2 buffer then needs NR-4 planes and each hand-off kind
+// NB = NR-4 barrier ids (planes whose hand-off can be outstanding at once)
+template <int TX_, int TY_, int NR = 6>
 struct TileWS {
     static constexpr int TX = TX_, TY = TY_, NT = TX * TY;
     static constexpr int R4X = TX + 8, R4Y = TY + 8, R4N = R4X * R4Y;
     static constexpr int R2X = TX + 4, R2Y = TY + 4, R2N = R2X * R2Y;
-    static constexpr int NRING = 6;
+    static constexpr int NRING = NR;
+    static constexpr int LBD = NR - 4;
+    static constexpr int NB = NR - 4 < 2 ? 2 : NR - 4;
+    static_assert(NR >= 6 && 2 + 3 * NB <= 16, "ring depth");
+    static __device__ __forceinline__ int slot(int p) { return (p + 8 * NR) % NR; }
+    static __device__ __forceinline__ int lbuf(int c) { return (c + 8 * LBD) % LBD; }
+    static __device__ __forceinline__ int bid(int base, int p) { return base + (p + 64) % NB; }
 };
 
 // shared-memory carve-up: 6-slot rings, a double level-2 buffer, staging
@@ -45,7 +54,7 @@ struct WsSmem {
     static constexpr size_t p_bytes = (size_t)4 * TL::NRING * TL::R4N * sizeof(PT);
     static constexpr size_t pp_bytes = (size_t)TL::NRING * TL::R2N * sizeof(PT);
     static constexpr size_t q_bytes = (size_t)5 * TL::NRING * TL::R2N * sizeof(RCt);
-    static constexpr size_t l_bytes = (size_t)2 * 5 * TL::R2N * sizeof(RCt);
+    static constexpr size_t l_bytes = (size_t)TL::LBD * 5 * TL::R2N * sizeof(RCt);
     static constexpr size_t s_off = (p_bytes + pp_bytes + q_bytes + l_bytes + 15) & ~(size_t)15;
     static constexpr size_t total = s_off + (size_t)5 * TL::R4N * sizeof(QS);
 };
@@ -56,13 +65,12 @@ __device__ __forceinline__ void nb_arrive(int id, int n) {
     __threadfence_block();
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-enum WsBar { WS_PROD = 1, WS_FULL = 2, WS_LREADY = 4, WS_EMPTY = 6, WS_FULLC = 8 };  // +0/+1 by plane parity
+// barrier ids: 1 producers only; then NB ids each for FULL, LREADY, EMPTY
+template <class TL>
+struct WsBar {
+    static constexpr int PROD = 1, FULL = 2, LREADY = 2 + TL::NB, EMPTY = 2 + 2 * TL::NB;
+};
 
-#ifndef MPFD_WS_OWNA
-#define MPFD_WS_OWNA 0
-#endif
-
-__device__ __forceinline__ int ring_slot(int p) { return (p + 12) % 6; }
 
 #ifndef MPFD_WS_PREG
 #define MPFD_WS_PREG 56
@@ -124,16 +132,14 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
     const WC2 rw = kget<WC2>(a.kb[K_R_STAGE]);
     const QS* qin = (const QS*)a.qin;
     constexpr int PF = TL::NRING * TL::R4N;
-    // OWNA: consumers compute phase A at their own pair (the tile interior);
-    // producers only on the 4-point ring around it
-    constexpr bool OWNA = MPFD_WS_OWNA != 0;
+    using BAR = WsBar<TL>;
     const WC2 half = kget<WC2>(a.kb[K_HALF]), gm1 = kget<WC2>(a.kb[K_GM1]), gM2 = kget<WC2>(a.kb[K_GM2]);
 
     // phase A of one point pair: staging pair index si, rim descriptor ri
     // (element index | R2 index << 13 | in R2 << 26 | owned interior << 27),
     // wrapped in-plane offset roff; copies plane p+1 into its staging entries
     auto a_pair = [&](int p, int si, unsigned ri, int roff) {
-        const int slot = ring_slot(p);
+        const int slot = TL::slot(p);
         const QS* sp = Sg + 2 * si;
         const QS2 q0 = ldv<QS>(sp), q1 = ldv<QS>(sp + TL::R4N), q2 = ldv<QS>(sp + 2 * TL::R4N),
                   q3 = ldv<QS>(sp + 3 * TL::R4N), q4 = ldv<QS>(sp + 4 * TL::R4N);
@@ -196,31 +202,15 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
         // ======================= producers ====================================
         if constexpr (PREG > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PREG));
         const int ptid = tid;
-        // this producer's rim pairs: the whole R4 box, or (OWNA) the ring of
-        // pairs around the tile interior
-        constexpr int NRIM = OWNA ? 8 * R4P + 4 * TL::TY : R4NP;
+        // this producer's rim pairs (the whole R4 box)
+        constexpr int NRIM = R4NP;
         constexpr int KPF = (NRIM + NP - 1) / NP;
         int rim_off[KPF], rsi[KPF];
         unsigned rinfo[KPF];
 #pragma unroll
         for (int k = 0; k < KPF; ++k) {
             const int j = min(ptid + k * NP, NRIM - 1);
-            int ry, pc;
-            if (!OWNA) {
-                ry = j / R4P;
-                pc = j - ry * R4P;
-            } else if (j < 4 * R4P) {
-                ry = j / R4P;
-                pc = j - ry * R4P;
-            } else if (j < 4 * R4P + 4 * TL::TY) {
-                const int kk = j - 4 * R4P, cc = kk & 3;
-                ry = 4 + (kk >> 2);
-                pc = cc < 2 ? cc : TXP + cc;
-            } else {
-                const int kk = j - 4 * R4P - 4 * TL::TY;
-                ry = TL::TY + 4 + kk / R4P;
-                pc = kk - (kk / R4P) * R4P;
-            }
+            const int ry = j / R4P, pc = j - ry * R4P;
             rsi[k] = ry * R4P + pc;
             rim_off[k] = wrap_off(2 * pc, ry);
             rinfo[k] = rim_desc(2 * pc, ry);
@@ -241,7 +231,7 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
         for (int p = zs - 4; p < ze + 4; ++p) {
             // A(p) overwrites the slot of plane p-6 (last read by C(p-4)); the
             // rim part of B(p-2) below overwrites the level-2 buffer of p-4
-            if (p >= zs + 2) nb_sync(WS_EMPTY + (p & 1), NALL);
+            if (p >= zs + TL::NRING - 4) nb_sync(TL::bid(BAR::EMPTY, p), NALL);
             cp_async_wait_all();
 #pragma unroll
             for (int k = 0; k < KPF; ++k) {
@@ -249,19 +239,16 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
                 a_pair(p, rsi[k], rinfo[k], rim_off[k]);
             }
             cp_async_commit();
-            if (p >= zs) nb_arrive(WS_FULL + (p & 1), NALL);
+            if (p >= zs) nb_arrive(TL::bid(BAR::FULL, p), NALL);
             // ---- rim part of B(p-2): needs A(p) of every producer ----
             const int cpl = p - 2;
-            // A(p) complete everywhere: producers (and, OWNA, consumers' own pairs)
-            if (cpl >= zs - 2 && cpl < ze + 2) {
-                if (OWNA) nb_sync(WS_FULLC + (p & 1), NALL);
-                else if (c.viscous) nb_sync(WS_PROD, NP);
-            }
+            // A(p) complete in every producer
             if (c.viscous && cpl >= zs - 2 && cpl < ze + 2) {
+                nb_sync(BAR::PROD, NP);
                 const PT* plp[5];
 #pragma unroll
-                for (int i = 0; i < 5; ++i) plp[i] = Pr + ring_slot(cpl - 2 + i) * TL::R4N;
-                T* Lb = Lbuf + (cpl & 1) * 5 * TL::R2N;
+                for (int i = 0; i < 5; ++i) plp[i] = Pr + TL::slot(cpl - 2 + i) * TL::R4N;
+                T* Lb = Lbuf + TL::lbuf(cpl) * 5 * TL::R2N;
                 constexpr int NXR = 2 * TL::TY, NYR = 4 * TXP;
                 for (int k = ptid; k < NXR + NYR; k += NP) {
                     int rx, ry, dir;
@@ -305,7 +292,7 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
                            ring_grad2<T2, WC2, PT, TL, STAGED>(plp, q4, 3, dir, c, rw, a.sc));
                 }
             }
-            if (cpl >= zs - 2 && cpl < ze + 2) nb_arrive(WS_LREADY + (cpl & 1), NALL);
+            if (cpl >= zs - 2 && cpl < ze + 2) nb_arrive(TL::bid(BAR::LREADY, cpl), NALL);
         }
         cp_async_wait_all();
         return;
@@ -326,23 +313,6 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
 #pragma unroll
     for (int i = 0; i < 5; ++i) wdiv[i] = wgz[i] = wdt[i] = Op<T2>::zero();
 
-    // OWNA: phase A at this thread's own pair (tile interior)
-    const int own_si = (ty + 4) * R4P + tx + 2;
-    const unsigned own_ri = rim_desc(2 * tx + 4, ty + 4);
-    const int own_off = wrap_off(2 * tx + 4, ty + 4);
-    if constexpr (OWNA) {
-        const QS* qb = qin + (long long)(zs - 4 + kHalo) * 5 * g.plane + own_off;
-#pragma unroll
-        for (int cc = 0; cc < 5; ++cc) cp_async<2 * sizeof(QS)>(Sg + cc * TL::R4N + 2 * own_si, qb + cc * g.plane);
-        cp_async_commit();
-        for (int p = zs - 4; p <= zs; ++p) {
-            cp_async_wait_all();
-            a_pair(p, own_si, own_ri, own_off);
-            cp_async_commit();
-        }
-        nb_arrive(WS_FULLC + (zs & 1), NALL);
-    }
-
     for (int cp = zs - 2; cp < ze + 2; ++cp) {
         // stage-update operands of the late residual (plane cp-2)
         const bool do_d = cp - 2 >= zs && cp - 2 < ze && own;
@@ -351,11 +321,11 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
             ind[0] = rk_load2<QS, TS>(a, 3, cp - 2, o);
             ind[1] = rk_load2<QS, TS>(a, 4, cp - 2, o);
         }
-        nb_sync(WS_FULL + ((cp + 2) & 1), NALL);  // A(cp+2) done: planes cp-2..cp+2 in the rings
+        nb_sync(TL::bid(BAR::FULL, cp + 2), NALL);  // A(cp+2) done: planes cp-2..cp+2 in the rings
         const PT* plp[5];
 #pragma unroll
-        for (int i = 0; i < 5; ++i) plp[i] = Pr + ring_slot(cp - 2 + i) * TL::R4N;
-        T* Lb = Lbuf + (cp & 1) * 5 * TL::R2N;
+        for (int i = 0; i < 5; ++i) plp[i] = Pr + TL::slot(cp - 2 + i) * TL::R4N;
+        T* Lb = Lbuf + TL::lbuf(cp) * 5 * TL::R2N;
         // ---- own part of B(cp) ----
         if (c.viscous) {
             T2 G[9], dT[3], u[3];
@@ -384,7 +354,7 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
             wgz[4] = gg[2];
             wdt[4] = dT[2];
         }
-        nb_sync(WS_LREADY + (cp & 1), NALL);  // level-2 of plane cp complete (own + rim)
+        nb_sync(TL::bid(BAR::LREADY, cp), NALL);  // level-2 of plane cp complete (own + rim)
         // ---- late residual of plane cp-2 -> RK of rhow, rhoE ----
         if (do_d) {
             T2 cw = Op<T2>::zero(), tz = Op<T2>::zero(), hz = Op<T2>::zero();
@@ -404,7 +374,7 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
             RingAcc2<T2, PT, TL> acc;
 #pragma unroll
             for (int i = 0; i < 5; ++i) {
-                const int s = ring_slot(cp - 2 + i);
+                const int s = TL::slot(cp - 2 + i);
                 acc.pp[i] = plp[i] + p4;
                 acc.prs[i] = Ppr + s * TL::R2N + p2;
                 acc.qp[i] = Qr + s * TL::R2N + p2;
@@ -419,17 +389,9 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
             for (int comp = 0; comp < 3; ++comp)
                 rk_pair<QS, TS, RS, TC, QC, TL>(a, comp, cp, o, cvt<RS2>(out[comp]), inc[comp], x, y);
         }
-        if constexpr (OWNA) {
-            // plane cp+3 at the own pair: its slot (plane cp-3) was last read
-            // by C(cp-1) and B(cp-1), both complete (LREADY(cp) above)
-            if (cp + 3 < ze + 4) {
-                cp_async_wait_all();
-                a_pair(cp + 3, own_si, own_ri, own_off);
-                cp_async_commit();
-                nb_arrive(WS_FULLC + ((cp + 3) & 1), NALL);
-            }
-        }
-        nb_arrive(WS_EMPTY + ((cp + 4) & 1), NALL);  // planes cp-2.. and level-2 of cp released
+        // releases plane cp-2's ring slot (reused by A(cp+NR-2)) and level-2
+        // buffer of plane cp (reused by the rim part of B(cp+NR-4))
+        nb_arrive(TL::bid(BAR::EMPTY, cp + TL::NRING - 2), NALL);
     }
     cp_async_wait_all();
 }
