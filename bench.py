@@ -258,6 +258,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_total = float(t.item())
         kms, klaunch = s.profile_read()
+        halo_sent = s.halo_bytes()
         s.profile(False)
         ms_step = ms_total / args.steps
         npts = n ** 3 * zper  # whole job
@@ -293,7 +294,20 @@ def main():
         if with_extras and not args.no_e2e:
             res["e2e"] = e2e_run(m, s, n, dt, args.steps, world, rank)
         dev, census, census64 = s.memory()
-        res["device_bytes"] = dev
+        bq_ = PRESET_KINDS[preset][0]
+        res["memory"] = {
+            "device_bytes": dev, "census_bytes": census, "census_b64_bytes": census64,
+            "census_gain": census64 / census if census else None,
+            "note": "device_bytes: HBM this solver holds (Q, Qt double-buffered, R); census: the "
+                    "reference's analytic memory_report of its field set (registry.cpp:24-39)"}
+        if use_nccl:
+            # measured ncclSend bytes per RK step vs comm_volume_report's model
+            # (registry.cpp:41-66; depth 2, q exchanged 3x per iteration)
+            steps_run = args.warmup + args.steps
+            res["halo"] = {"measured_bytes_per_step": halo_sent / steps_run,
+                           "model_bytes_per_step": (2 * 2 * n * n * bq_ * 3 * 5 if world > 1 else 0),
+                           "note": "we exchange Q only, 4 ghost planes deep (primitives and "
+                                   "gradients are rebuilt from ghost Q), in q storage precision"}
         s.close()
         del s
         torch.cuda.synchronize()
@@ -331,6 +345,7 @@ def main():
             "b_alg": {"bytes_per_pt_per_step": head["b_alg_bytes_per_pt"],
                       "frac_of_hbm": head["b_alg_frac"]},
             "gpu_launches": head["gpu_launches"],
+            "memory": head.get("memory"),
             "clocks": head["clocks"],
             "kernel_ms": head["kernel_ms"],
             "per_precision": {args.precision: {"value": head["value"],
@@ -339,6 +354,8 @@ def main():
         }
         if "e2e" in head:
             line["e2e"] = head["e2e"]
+        if "halo" in head:
+            line["halo"] = head["halo"]
         if not args.no_cpu_baseline and world == 1:
             try:
                 rate, cores, kind, sample = cpu_reference_run(args.precision, args.strategy,

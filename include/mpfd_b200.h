@@ -197,6 +197,15 @@ int mpfd_b200_memory(mpfd_solver* s, size_t* device_bytes, size_t* census_bytes,
  * out[9] = {send_up, recv_lo, send_dn, recv_hi, block_bytes, up, dn, z0, nzl}. */
 int mpfd_b200_halo_plan(int n, int pz, int rank, int bytes_q, long long out[9]);
 
+/* PrecisionConfig::resolve (precision.cpp:46-56): storage kind of field
+ * `name` of class `cls` (MPFD_Q_VECTOR..; 4 = diagnostics, pinned to B64)
+ * under `prec`, per-name overrides first.  Pure host arithmetic: what the
+ * reference's memory_report / comm_volume_report (registry.cpp:24-66) need. */
+int mpfd_b200_field_kind(const mpfd_precision* prec, int cls, const char* name, int* kind);
+/* Bytes this rank has handed to ncclSend for halo exchanges since creation
+ * (the measured counterpart of comm_volume_report, registry.cpp:41-66). */
+int mpfd_b200_halo_bytes(mpfd_solver* s, unsigned long long* sent);
+
 /* Which residual path runs: 0 = staged multi-kernel, 1 = fused. */
 int mpfd_b200_set_path(mpfd_solver* s, int path);
 /* Overlap of the z-halo exchange with the interior planes (fused path,

@@ -149,6 +149,7 @@ static double tree_of_chunks(const double* c, size_t n) {
 
 // ---------------------------------------------------------------------------
 struct Solver {
+    unsigned long long halo_sent = 0;  // bytes handed to ncclSend by this rank
     // configuration
     int n = 0;
     int zper = 1, nzg = 0;  // z periods (weak scaling) and global z planes n * zper
@@ -649,6 +650,7 @@ void Solver::halo_refresh() {
         Nccl& nc = Nccl::get();
         timed(2, s, [&] {
             nc.check(nc.groupStart(), "ncclGroupStart");
+            halo_sent += 2 * blk;
             nc.check(nc.send(top_int, blk, 1, up, comm, s.stream), "ncclSend");
             nc.check(nc.recv(lo_ghost, blk, 1, dn, comm, s.stream), "ncclRecv");
             nc.check(nc.send(bot_int, blk, 1, dn, comm, s.stream), "ncclSend");
@@ -738,6 +740,7 @@ void Solver::exchange_async() {
         const size_t blk = (size_t)hp.block;
         Nccl& nc = Nccl::get();
         nc.check(nc.groupStart(), "ncclGroupStart");
+        halo_sent += 2 * blk;
         nc.check(nc.send(q + hp.send_up, blk, 1, hp.up, comm, s.comm), "ncclSend");
         nc.check(nc.recv(q + hp.recv_lo, blk, 1, hp.dn, comm, s.comm), "ncclRecv");
         nc.check(nc.send(q + hp.send_dn, blk, 1, hp.dn, comm, s.comm), "ncclSend");
@@ -1410,6 +1413,35 @@ int mpfd_b200_memory(mpfd_solver* h, size_t* device_bytes, size_t* census, size_
             }
         if (census) *census = tot;
         if (census_b64) *census_b64 = cnt * pts * 8;
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_field_kind(const mpfd_precision* p, int cls, const char* name, int* kind) {
+    return guard([&] {
+        if (!p || !name || !kind) throw ConfigError("null argument");
+        // PrecisionConfig::resolve (precision.cpp:46-56): a per-name override
+        // wins; diagnostics are pinned to B64
+        for (int i = 0; i < p->n_overrides; ++i)
+            if (std::string(p->override_names[i]) == name) {
+                *kind = p->override_kinds[i];
+                return MPFD_OK;
+            }
+        switch (cls) {
+            case 0: *kind = p->q_vector; break;
+            case 1: *kind = p->rk_arrays; break;
+            case 2: *kind = p->residuals; break;
+            case 3: *kind = p->wk_arrays; break;
+            default: *kind = 2;
+        }
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_halo_bytes(mpfd_solver* h, unsigned long long* sent) {
+    return guard([&] {
+        if (!sent) throw ConfigError("null argument");
+        *sent = h->s.halo_sent;
         return MPFD_OK;
     });
 }

@@ -127,6 +127,8 @@ def lib():
         L.mpfd_b200_run_steps.argtypes = [P, C.POINTER(_Step), C.c_long]
         L.mpfd_b200_profile.argtypes = [P, I]
         L.mpfd_b200_profile_read.argtypes = [P, DP, C.POINTER(C.c_long)]
+        L.mpfd_b200_halo_bytes.argtypes = [P, C.POINTER(C.c_ulonglong)]
+        L.mpfd_b200_field_kind.argtypes = [P, I, C.c_char_p, C.POINTER(I)]
         L.mpfd_b200_memory.argtypes = [P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
                                        C.POINTER(C.c_size_t)]
         L.mpfd_b200_set_path.argtypes = [P, I]
@@ -452,6 +454,12 @@ class Solver:
         a, b, c = C.c_size_t(), C.c_size_t(), C.c_size_t()
         _check(self.L.mpfd_b200_memory(self.h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
+
+    def halo_bytes(self) -> int:
+        """Bytes this rank handed to ncclSend for halo exchanges so far."""
+        v = C.c_ulonglong()
+        _check(self.L.mpfd_b200_halo_bytes(self.h, C.byref(v)))
+        return v.value
 
     def set_path(self, path: str):
         _check(self.L.mpfd_b200_set_path(self.h, 1 if path == "fused" else 0))

@@ -120,3 +120,29 @@ def test_sweep_matrix_identical(b200, tmp_path):
         outs[who] = (r.stdout.replace(who + ".csv", "X.csv"), (tmp_path / f"{who}.csv").read_bytes())
     assert outs["ref"] == outs["b200"]
     assert outs["ref"][1].count(b"\n") == 5
+
+
+REPORTS = {
+    "dp_default": "n = 64\n",
+    "hpsp_default_pencils": "n = 64\nprecision = HPSP\nprocs = 1,2,4\n",
+    "spdp_storesome_slabs": "n = 128\nprecision = SPDP\nstrategy = storesome\nprocs = 1,1,8\n",
+    "spdp_res_override": "n = 32\nprecision = SPDP-res\nprecision.custom.u = B16\nprecision.custom.dTdz = B32\n"
+                         "procs = 2,2,2\ncomm.rk_arrays = 1\ncomm.wk_arrays = 2\n",
+    "hp_pencils": "n = 96\nprecision = HP\nprocs = 2,2,2\n",
+    "bad_procs": "n = 30\nprocs = 1,1,4\n",
+}
+
+
+@pytest.mark.skipif(not os.path.exists(REF_CLI), reason="reference CLI not built")
+@pytest.mark.parametrize("name", list(REPORTS))
+def test_report_identical(b200, tmp_path, name):
+    """`report <config>` (print_report, runner.cpp:90-106): the analytic memory
+    census of the field set and the modelled halo volume per process, byte for
+    byte the reference CLI's (and the same exit code on a bad process grid)."""
+    tool = build_tool(b200)
+    cfg = tmp_path / "r.cfg"
+    cfg.write_text(REPORTS[name])
+    r1 = subprocess.run([REF_CLI, "report", str(cfg)], capture_output=True, text=True)
+    r2 = subprocess.run([tool, "report", str(cfg)], capture_output=True, text=True)
+    assert r1.returncode == r2.returncode
+    assert r1.stdout == r2.stdout

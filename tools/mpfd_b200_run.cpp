@@ -1,5 +1,5 @@
 // mpfd_b200_run -- the reference CLI's `run`, `compare` and `sweep` commands
-// (tools/mpfd.cpp:23-46; runner.cpp:69-88, 108-173) on the B200 path, through
+// (tools/mpfd.cpp:23-52; runner.cpp:69-173) and `report` on the B200 path, through
 // the C++ adapter (include/mpfd_b200.hpp).
 //
 // Reads the reference's `key = value` config (config.cpp:120-235, the keys
@@ -47,6 +47,9 @@ struct Cfg {
     std::vector<std::string> sweep_presets;
     std::string sweep_output;
     bool saw_t_end = false;
+    // report (config.cpp:190-205)
+    int procs[3] = {4, 1, 1};  // SimConfig default (config.hpp:33)
+    double comm[4] = {-1, -1, -1, -1};  // comm.q_vector / rk_arrays / residuals / wk_arrays
 };
 
 std::vector<std::string> split_list(const std::string& key, const std::string& v, int ln) {
@@ -106,6 +109,17 @@ Cfg load(const std::string& path, bool sweep = false) {
             for (const auto& pr : c.sweep_presets) mpfd_b200::resolve_preset(pr.c_str());  // validate
         }
         else if (sweep && k == "sweep.output") c.sweep_output = v;
+        else if (k == "procs") {
+            const auto l = split_list(k, v, ln);
+            if (l.size() != 3)
+                throw mpfd_b200::ConfigError("line " + std::to_string(ln) + ": field 'procs': expected px,py,pz");
+            for (int i = 0; i < 3; ++i) c.procs[i] = std::stoi(l[i]);
+        }
+        else if (k == "comm.q_vector") c.comm[0] = std::stod(v);
+        else if (k == "comm.rk_arrays") c.comm[1] = std::stod(v);
+        else if (k == "comm.residuals") c.comm[2] = std::stod(v);
+        else if (k == "comm.wk_arrays") c.comm[3] = std::stod(v);
+        else if (k == "snapshot_times" || k == "snapshot_path") {}  // snapshots: not on the hot path
         else throw mpfd_b200::ConfigError("line " + std::to_string(ln) + ": unknown key '" + k + "'");
     }
     if (sweep && c.sweep_presets.empty()) throw mpfd_b200::ConfigError("sweep spec: missing 'sweep.presets'");
@@ -129,21 +143,30 @@ struct Run {
     mpfd_b200::AdvanceResult raw;
 };
 
-// run_simulation (runner.cpp:11-48) on cuda:0
-Run run_cfg(const Cfg& c) {
-    mpfd_precision p = mpfd_b200::resolve_preset(c.precision.c_str());
-    p.emulation = c.emulation == "storeround" ? MPFD_STOREROUND : MPFD_STRICT;
+// the resolved PrecisionConfig of a config (preset + per-name overrides)
+struct Prec {
+    mpfd_precision p;
     std::vector<std::string> names;
     std::vector<const char*> np;
     std::vector<int> kinds;
-    for (const auto& kv : c.custom) {
-        names.push_back(kv.first);
-        kinds.push_back(kv.second == "B16" ? MPFD_B16 : kv.second == "B32" ? MPFD_B32 : MPFD_B64);
+    explicit Prec(const Cfg& c) {
+        p = mpfd_b200::resolve_preset(c.precision.c_str());
+        p.emulation = c.emulation == "storeround" ? MPFD_STOREROUND : MPFD_STRICT;
+        for (const auto& kv : c.custom) {
+            names.push_back(kv.first);
+            kinds.push_back(kv.second == "B16" ? MPFD_B16 : kv.second == "B32" ? MPFD_B32 : MPFD_B64);
+        }
+        for (const auto& s : names) np.push_back(s.c_str());
+        p.n_overrides = (int)names.size();
+        p.override_names = np.data();
+        p.override_kinds = kinds.data();
     }
-    for (const auto& s : names) np.push_back(s.c_str());
-    p.n_overrides = (int)names.size();
-    p.override_names = np.data();
-    p.override_kinds = kinds.data();
+};
+
+// run_simulation (runner.cpp:11-48) on cuda:0
+Run run_cfg(const Cfg& c) {
+    const Prec pr(c);
+    const mpfd_precision& p = pr.p;
     const mpfd_flow flow{c.M, c.Re, c.Pr, c.gamma, c.viscous ? 1 : 0};
     mpfd_b200::Solver s(c.n, p, c.strategy == "storesome" ? MPFD_STORESOME : MPFD_DEFAULT, flow,
                         mpfd_b200::split_preset(c.split.c_str()));
@@ -313,6 +336,83 @@ int cmd_sweep(const char* path) {
     return 0;
 }
 
+// print_report (runner.cpp:90-106): the analytic memory census of
+// make_solver_fields' set (physics.cpp:441-475, memory_report registry.cpp:24-39)
+// and the modelled halo volume (comm_volume_report registry.cpp:41-66) with
+// the exchange counts of config.cpp:9-17; no run
+int cmd_report(const char* path) {
+    const Cfg c = load(path);
+    const Prec pr(c);
+    struct F {
+        const char* name;
+        int cls;
+    };
+    std::vector<F> fields;
+    static const char* qn[5] = {"rho", "rhou", "rhov", "rhow", "rhoE"};
+    static const char* tn[5] = {"rk_rho", "rk_rhou", "rk_rhov", "rk_rhow", "rk_rhoE"};
+    static const char* rn[5] = {"res_rho", "res_rhou", "res_rhov", "res_rhow", "res_rhoE"};
+    static const char* wn[5] = {"u", "v", "w", "p", "T"};
+    static const char* gn[12] = {"dudx", "dudy", "dudz", "dvdx", "dvdy", "dvdz",
+                                 "dwdx", "dwdy", "dwdz", "dTdx", "dTdy", "dTdz"};
+    for (auto n : qn) fields.push_back({n, 0});
+    for (auto n : tn) fields.push_back({n, 1});
+    for (auto n : rn) fields.push_back({n, 2});
+    for (auto n : wn) fields.push_back({n, 3});
+    if (c.strategy != "storesome")
+        for (auto n : gn) fields.push_back({n, 3});
+    const size_t ext = (size_t)c.n + 8, pts = ext * ext * ext;
+    size_t cnt[5] = {0}, bytes[5] = {0}, total = 0, base = 0;
+    std::vector<int> kinds;
+    for (const auto& f : fields) {
+        int k = 2;
+        if (mpfd_b200_field_kind(&pr.p, f.cls, f.name, &k)) throw mpfd_b200::ConfigError(mpfd_b200_last_error());
+        kinds.push_back(k);
+        const size_t b = pts * (k == 0 ? 2 : k == 1 ? 4 : 8);
+        ++cnt[f.cls];
+        bytes[f.cls] += b;
+        total += b;
+        base += pts * 8;
+    }
+    static const char* names[5] = {"q_vector", "rk_arrays", "residuals", "wk_arrays", "diagnostics"};
+    std::cout << "memory census (analytic, halos included):\n";
+    for (int k = 0; k < 5; ++k) {
+        if (cnt[k] == 0) continue;
+        std::cout << "  " << names[k] << ": " << cnt[k] << " fields, " << bytes[k] << " bytes\n";
+    }
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%.4f", total == 0 ? 1.0 : (double)base / (double)total);
+    std::cout << "  total: " << total << " bytes (all-B64 baseline " << base << " bytes, gain " << buf << "x)\n";
+    // exchange counts (config.cpp:9-17) and the face model, depth 2
+    const double counts[5] = {c.comm[0] >= 0 ? c.comm[0] : 3.0, c.comm[1] >= 0 ? c.comm[1] : 0.0,
+                              c.comm[2] >= 0 ? c.comm[2] : 0.0,
+                              c.comm[3] >= 0 ? c.comm[3] : (c.strategy != "storesome" ? 3.0 : 0.0), 0.0};
+    const int px = c.procs[0], py = c.procs[1], pz = c.procs[2];
+    double per[5] = {0}, tot = 0.0;
+    for (size_t i = 0; i < fields.size(); ++i) {
+        const int n = c.n;
+        if (px < 1 || py < 1 || pz < 1) throw mpfd_b200::ConfigError("process grid dimensions must be >= 1");
+        if (n % px != 0 || n % py != 0 || n % pz != 0)
+            throw mpfd_b200::ConfigError("grid n=" + std::to_string(n) + " is not divisible by the process grid");
+        const double lx = (double)n / px, ly = (double)n / py, lz = (double)n / pz;
+        double faces = 0.0;
+        if (px > 1) faces += ly * lz;
+        if (py > 1) faces += lx * lz;
+        if (pz > 1) faces += lx * ly;
+        const int k = kinds[i];
+        const double vol = 2.0 * 2 * faces * (k == 0 ? 2 : k == 1 ? 4 : 8) * counts[fields[i].cls];
+        per[fields[i].cls] += vol;
+        tot += vol;
+    }
+    std::cout << "modeled halo-exchange volume per process per iteration (procs " << px << "x" << py << "x" << pz
+              << "):\n";
+    for (int k = 0; k < 5; ++k) {
+        if (per[k] == 0.0) continue;
+        std::cout << "  " << names[k] << ": " << per[k] << " bytes\n";
+    }
+    std::cout << "  total: " << tot << " bytes\n";
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -321,8 +421,9 @@ int main(int argc, char** argv) {
         if (cmd == "run" && argc == 3) return cmd_run(argv[2]);
         if (cmd == "compare" && argc == 4) return cmd_compare(argv[2], argv[3]);
         if (cmd == "sweep" && argc == 3) return cmd_sweep(argv[2]);
+        if (cmd == "report" && argc == 3) return cmd_report(argv[2]);
         std::cerr << "usage:\n  mpfd_b200_run run <config>\n  mpfd_b200_run compare <a.csv> <b.csv>\n"
-                     "  mpfd_b200_run sweep <spec>\n";
+                     "  mpfd_b200_run sweep <spec>\n  mpfd_b200_run report <config>\n";
         return 1;
     } catch (const mpfd_b200::ConfigError& e) {
         std::cerr << "error: " << e.what() << "\n";
