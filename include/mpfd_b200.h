@@ -172,6 +172,15 @@ int mpfd_b200_diagnostics(mpfd_solver* s, int weighting, double t, int threads, 
 int mpfd_b200_advance(mpfd_solver* s, const mpfd_step* step, mpfd_diag* series, long cap,
                       long* len, mpfd_divergence* ev, long* iters);
 
+/* write_snapshot (io.cpp:69-85): int32 {n, n, n, 5} then the five conserved
+ * components as binary64 n^3 arrays (i fastest).  Whole state in this
+ * process only (one slab or LOCAL slabs, z_periods 1). */
+int mpfd_b200_write_snapshot(mpfd_solver* s, const char* path);
+/* Snapshot schedule of advance (integrate.cpp:154-158, runner.cpp:34-41):
+ * after the iteration with t_next >= times[k] - dt/2, write
+ * <path without ".bin">_t<%.6g of t_next>.bin; path NULL = "snapshot.bin". */
+int mpfd_b200_set_snapshots(mpfd_solver* s, const double* times, int count, const char* path);
+
 /* --- measurement hooks (bench.py) --------------------------------------- */
 /* The solver's CUDA stream (cudaStream_t) for external event timing. */
 void* mpfd_b200_stream(mpfd_solver* s);

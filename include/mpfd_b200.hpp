@@ -124,6 +124,12 @@ class Solver {
         return r;
     }
 
+    // write_snapshot (io.cpp:69-85) and advance's snapshot schedule (runner.cpp:34-41)
+    void write_snapshot(const char* path) { check(mpfd_b200_write_snapshot(s_, path)); }
+    void set_snapshots(const std::vector<double>& times, const char* path) {
+        check(mpfd_b200_set_snapshots(s_, times.data(), (int)times.size(), path));
+    }
+
     mpfd_solver* handle() const { return s_; }
 
   private:

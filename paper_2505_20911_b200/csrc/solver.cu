@@ -150,6 +150,8 @@ static double tree_of_chunks(const double* c, size_t n) {
 // ---------------------------------------------------------------------------
 struct Solver {
     unsigned long long halo_sent = 0;  // bytes handed to ncclSend by this rank
+    std::vector<double> snap_times;    // advance's snapshot schedule (runner.cpp:34-41)
+    std::string snap_path = "snapshot.bin";
     // configuration
     int n = 0;
     int zper = 1, nzg = 0;  // z periods (weak scaling) and global z planes n * zper
@@ -1280,6 +1282,43 @@ static void check_step(const mpfd_step* st) {
     if (!(st->dt > 0)) throw ConfigError("dt must be positive");
 }
 
+// write_snapshot (io.cpp:69-85): int32 {n, n, n, 5}, then the five
+// conserved components as binary64, i fastest
+static void write_snapshot(Solver& S, const std::string& path) {
+    if (S.mode == MPFD_DECOMP_NCCL || S.zper != 1)
+        throw ConfigError("snapshots need the whole n^3 state in this process");
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw ConfigError("cannot open for writing: " + path);
+    const int32_t hdr[4] = {S.n, S.n, S.n, 5};
+    const size_t n = (size_t)S.n;
+    std::vector<double> buf(n * n * n);
+    bool ok = std::fwrite(hdr, sizeof hdr, 1, f) == 1;
+    for (int c = 0; c < 5 && ok; ++c) {
+        S.get_interior(0, c, buf.data(), n, n * n, 0);
+        ok = std::fwrite(buf.data(), sizeof(double), buf.size(), f) == buf.size();
+    }
+    std::fclose(f);
+    if (!ok) throw ConfigError("write failed: " + path);
+}
+
+int mpfd_b200_write_snapshot(mpfd_solver* h, const char* path) {
+    return guard([&] {
+        if (!path) throw ConfigError("null path");
+        h->s.sync();
+        write_snapshot(h->s, path);
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_set_snapshots(mpfd_solver* h, const double* times, int count, const char* path) {
+    return guard([&] {
+        if (count < 0 || (count > 0 && !times)) throw ConfigError("bad snapshot schedule");
+        h->s.snap_times.assign(times, times + count);
+        h->s.snap_path = path ? path : "snapshot.bin";
+        return MPFD_OK;
+    });
+}
+
 int mpfd_b200_advance(mpfd_solver* h, const mpfd_step* st, mpfd_diag* series, long cap, long* len,
                       mpfd_divergence* ev, long* iters) {
     return guard([&] {
@@ -1304,12 +1343,16 @@ int mpfd_b200_advance(mpfd_solver* h, const mpfd_step* st, mpfd_diag* series, lo
         int status = MPFD_OK;
         mpfd_divergence e{};
         const bool multi = S.mode == MPFD_DECOMP_NCCL;
+        size_t next_snap = 0;
         for (long it = 0; it < st->n_iterations; ++it) {
             const bool last = it + 1 == st->n_iterations;
+            const double t_next = (double)(it + 1) * st->dt;
             for (int sub = 0; sub < 3; ++sub)
                 S.substep_enqueue(sub, st->a, st->b, st->dt, (int)it, last && sub == 2);
             const bool due = st->diagnostics_interval > 0 && (it + 1) % st->diagnostics_interval == 0;
-            const bool check = due || last || (!multi && (it % 8) == 7) || (multi && (it % 64) == 63);
+            // snapshot rule of advance (integrate.cpp:154-158)
+            const bool snap = next_snap < S.snap_times.size() && t_next >= S.snap_times[next_snap] - 0.5 * st->dt;
+            const bool check = due || last || snap || (!multi && (it % 8) == 7) || (multi && (it % 64) == 63);
             if (check && S.poll_div(true)) {
                 S.resolve_div(&e, st->dt);
                 status = MPFD_DIVERGED;
@@ -1336,6 +1379,17 @@ int mpfd_b200_advance(mpfd_solver* h, const mpfd_step* st, mpfd_diag* series, lo
             }
             done = it + 1;
             if (due) sample((it + 1) * st->dt, false);
+            if (snap) {
+                // snapshot_path with ".bin" stripped + "_t%.6g.bin" (runner.cpp:34-41)
+                char suffix[32];
+                std::snprintf(suffix, sizeof suffix, "_t%.6g.bin", t_next);
+                std::string path = S.snap_path;
+                const auto dot = path.rfind(".bin");
+                if (dot != std::string::npos && dot == path.size() - 4) path.resize(dot);
+                S.sync();
+                write_snapshot(S, path + suffix);
+                ++next_snap;
+            }
         }
         S.sync();
         if (len) *len = count;

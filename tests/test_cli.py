@@ -146,3 +146,24 @@ def test_report_identical(b200, tmp_path, name):
     r2 = subprocess.run([tool, "report", str(cfg)], capture_output=True, text=True)
     assert r1.returncode == r2.returncode
     assert r1.stdout == r2.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(REF_CLI), reason="reference CLI not built")
+def test_snapshots_identical(b200, tmp_path):
+    """snapshot_times / snapshot_path (advance integrate.cpp:154-158, runner.cpp:
+    34-41, write_snapshot io.cpp:69-85): the same files, byte for byte."""
+    tool = build_tool(b200)
+    base = ("n = 24\nprecision = HPSP\nM = 0.1\nRe = 1600\ndt = 0.002\nn_iterations = 30\n"
+            "diagnostics_interval = 10\nstrategy = storesome\nsnapshot_times = 0.01, 0.035, 0.06\n")
+    files = {}
+    for who, exe in (("ref", REF_CLI), ("b200", tool)):
+        d = tmp_path / who
+        d.mkdir()
+        (d / "c.cfg").write_text(base + f"snapshot_path = {d / 'snap.bin'}\noutput = {d / 'o.csv'}\n")
+        r = subprocess.run([exe, "run", str(d / "c.cfg")], capture_output=True, text=True, cwd=d)
+        assert r.returncode == 0, r.stderr
+        files[who] = {p.name: p.read_bytes() for p in d.iterdir() if p.name.startswith("snap")}
+    assert sorted(files["ref"]) == sorted(files["b200"]) and len(files["ref"]) == 3
+    for k in files["ref"]:
+        assert files["ref"][k] == files["b200"][k], k

@@ -49,6 +49,8 @@ struct Cfg {
     bool saw_t_end = false;
     // report (config.cpp:190-205)
     int procs[3] = {4, 1, 1};  // SimConfig default (config.hpp:33)
+    std::vector<double> snap_times;
+    std::string snap_path = "snapshot.bin";
     double comm[4] = {-1, -1, -1, -1};  // comm.q_vector / rk_arrays / residuals / wk_arrays
 };
 
@@ -119,7 +121,8 @@ Cfg load(const std::string& path, bool sweep = false) {
         else if (k == "comm.rk_arrays") c.comm[1] = std::stod(v);
         else if (k == "comm.residuals") c.comm[2] = std::stod(v);
         else if (k == "comm.wk_arrays") c.comm[3] = std::stod(v);
-        else if (k == "snapshot_times" || k == "snapshot_path") {}  // snapshots: not on the hot path
+        else if (k == "snapshot_times") { for (auto& x : split_list(k, v, ln)) c.snap_times.push_back(std::stod(x)); }
+        else if (k == "snapshot_path") c.snap_path = v;
         else throw mpfd_b200::ConfigError("line " + std::to_string(ln) + ": unknown key '" + k + "'");
     }
     if (sweep && c.sweep_presets.empty()) throw mpfd_b200::ConfigError("sweep spec: missing 'sweep.presets'");
@@ -175,6 +178,7 @@ Run run_cfg(const Cfg& c) {
     mpfd_step st = mpfd_b200::default_step(c.dt, c.n_iter, c.diag_interval);
     st.ke_weighting = c.ke == "density" ? MPFD_KE_DENSITY : MPFD_KE_PLAIN;
     st.threads = c.threads;
+    if (!c.snap_times.empty()) s.set_snapshots(c.snap_times, c.snap_path.c_str());
     Run r;
     r.raw = s.advance(st);
     r.series = r.raw.series;
