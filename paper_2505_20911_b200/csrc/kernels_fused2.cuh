@@ -555,19 +555,25 @@ struct FusedPlan {
 #define MPFD_WS_NPW 8
 #endif
 #ifndef MPFD_WS32
-#define MPFD_WS32 0
+#define MPFD_WS32 1
 #endif
 #ifndef MPFD_WS32_NPW
-#define MPFD_WS32_NPW 4
+#define MPFD_WS32_NPW 8
 #endif
 #ifndef MPFD_WS32_TY
-#define MPFD_WS32_TY 8
+#define MPFD_WS32_TY 16
 #endif
 #ifndef MPFD_WS_NR
 #define MPFD_WS_NR 6
 #endif
-    using TLW = typename std::conditional<sizeof(T) == 2, TileWS<64, MPFD_WS_TY, MPFD_WS_NR>,
-                                          TileWS<32, MPFD_WS32_TY>>::type;
+#ifndef MPFD_WS32_STAGE
+#define MPFD_WS32_STAGE 0
+#endif
+#ifndef MPFD_WS_STAGE
+#define MPFD_WS_STAGE 1
+#endif
+    using TLW = typename std::conditional<sizeof(T) == 2, TileWS<64, MPFD_WS_TY, MPFD_WS_NR, MPFD_WS_STAGE != 0>,
+                                          TileWS<32, MPFD_WS32_TY, 6, MPFD_WS32_STAGE != 0>>::type;
     static constexpr int NPW = sizeof(T) == 2 ? MPFD_WS_NPW : MPFD_WS32_NPW;
     static constexpr bool WS = MPFD_WS != 0 && PAIR && (sizeof(T) == 2 || MPFD_WS32 != 0) &&
                                WsSmem<TLW, T, PT, QS>::total <= 232448;

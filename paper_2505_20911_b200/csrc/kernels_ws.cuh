@@ -34,8 +34,11 @@ namespace mpfd_b200 {
 // NR ring slots (>= 6): A(p) may run NR-6 planes further ahead of the
 // residual; the level-2 buffer then needs NR-4 planes and each hand-off kind
 // NB = NR-4 barrier ids (planes whose hand-off can be outstanding at once)
-template <int TX_, int TY_, int NR = 6>
+template <int TX_, int TY_, int NR = 6, bool STG = true>
 struct TileWS {
+    // STG: next plane's Q staged by cp.async; otherwise producers load it
+    // from global memory, prefetched into L2 two planes ahead
+    static constexpr bool STAGE = STG;
     static constexpr int TX = TX_, TY = TY_, NT = TX * TY;
     static constexpr int R4X = TX + 8, R4Y = TY + 8, R4N = R4X * R4Y;
     static constexpr int R2X = TX + 4, R2Y = TY + 4, R2N = R2X * R2Y;
@@ -56,7 +59,7 @@ struct WsSmem {
     static constexpr size_t q_bytes = (size_t)5 * TL::NRING * TL::R2N * sizeof(RCt);
     static constexpr size_t l_bytes = (size_t)TL::LBD * 5 * TL::R2N * sizeof(RCt);
     static constexpr size_t s_off = (p_bytes + pp_bytes + q_bytes + l_bytes + 15) & ~(size_t)15;
-    static constexpr size_t total = s_off + (size_t)5 * TL::R4N * sizeof(QS);
+    static constexpr size_t total = s_off + (TL::STAGE ? (size_t)5 * TL::R4N * sizeof(QS) : 0);
 };
 
 __device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -76,7 +79,7 @@ struct WsBar {
 #define MPFD_WS_PREG 56
 #endif
 #ifndef MPFD_WS32_PREG
-#define MPFD_WS32_PREG 0
+#define MPFD_WS32_PREG 64
 #endif
 // register split between the roles: producer warpgroups shrink to PREG
 // registers per thread (setmaxnreg.dec) and consumers grow to CREG
@@ -140,13 +143,28 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
     // wrapped in-plane offset roff; copies plane p+1 into its staging entries
     auto a_pair = [&](int p, int si, unsigned ri, int roff) {
         const int slot = TL::slot(p);
-        const QS* sp = Sg + 2 * si;
-        const QS2 q0 = ldv<QS>(sp), q1 = ldv<QS>(sp + TL::R4N), q2 = ldv<QS>(sp + 2 * TL::R4N),
-                  q3 = ldv<QS>(sp + 3 * TL::R4N), q4 = ldv<QS>(sp + 4 * TL::R4N);
+        QS2 q0, q1, q2, q3, q4;
+        if constexpr (TL::STAGE) {
+            const QS* sp = Sg + 2 * si;
+            q0 = ldv<QS>(sp), q1 = ldv<QS>(sp + TL::R4N), q2 = ldv<QS>(sp + 2 * TL::R4N),
+            q3 = ldv<QS>(sp + 3 * TL::R4N), q4 = ldv<QS>(sp + 4 * TL::R4N);
+        } else {
+            const QS* gp = qin + (long long)(p + kHalo) * 5 * g.plane + roff;
+            q0 = __ldg(reinterpret_cast<const QS2*>(gp));
+            q1 = __ldg(reinterpret_cast<const QS2*>(gp + g.plane));
+            q2 = __ldg(reinterpret_cast<const QS2*>(gp + 2 * g.plane));
+            q3 = __ldg(reinterpret_cast<const QS2*>(gp + 3 * g.plane));
+            q4 = __ldg(reinterpret_cast<const QS2*>(gp + 4 * g.plane));
+            if (p + 2 < ze + 4) {
+                const QS* gn = gp + 2 * 5 * g.plane;
+#pragma unroll
+                for (int cc = 0; cc < 5; ++cc) asm volatile("prefetch.global.L2 [%0];" ::"l"(gn + cc * g.plane));
+            }
+        }
         const WC2 rho = cvt<WC2>(q0);
         const PrimOut<WC2> pv =
             PrimCalc<WC2>::run(rho, cvt<WC2>(q1), cvt<WC2>(q2), cvt<WC2>(q3), cvt<WC2>(q4), half, gm1, gM2);
-        if (p + 1 < ze + 4) {
+        if (TL::STAGE && p + 1 < ze + 4) {
             // this thread's staging entries were consumed (their loads fed the
             // primitives above): copy plane p+1 into them
             const QS* qb = qin + (long long)(p + 1 + kHalo) * 5 * g.plane + roff;
@@ -216,7 +234,7 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
             rinfo[k] = rim_desc(2 * pc, ry);
         }
         // each producer thread copies exactly the staging entries it reads
-        {
+        if constexpr (TL::STAGE) {
             const QS* qb = qin + (long long)(zs - 4 + kHalo) * 5 * g.plane;
 #pragma unroll
             for (int k = 0; k < KPF; ++k) {
