@@ -155,8 +155,11 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
             q2 = __ldg(reinterpret_cast<const QS2*>(gp + 2 * g.plane));
             q3 = __ldg(reinterpret_cast<const QS2*>(gp + 3 * g.plane));
             q4 = __ldg(reinterpret_cast<const QS2*>(gp + 4 * g.plane));
-            if (p + 2 < ze + 4) {
-                const QS* gn = gp + 2 * 5 * g.plane;
+#ifndef MPFD_WS_PFD
+#define MPFD_WS_PFD 2
+#endif
+            if (p + MPFD_WS_PFD < ze + 4) {
+                const QS* gn = gp + MPFD_WS_PFD * 5 * g.plane;
 #pragma unroll
                 for (int cc = 0; cc < 5; ++cc) asm volatile("prefetch.global.L2 [%0];" ::"l"(gn + cc * g.plane));
             }
