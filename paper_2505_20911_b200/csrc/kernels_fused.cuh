@@ -184,7 +184,7 @@ __device__ __forceinline__ RkIn<QS, TS> rk_load(const FusedArgs& a, int comp, in
 // residual, 1 before it (registers live across the residual), 2 after it
 // with an L2 prefetch issued at the start of the iteration
 #ifndef MPFD_RKC
-#define MPFD_RKC 1
+#define MPFD_RKC 2
 #endif
 #ifndef MPFD_RAW_PF
 #define MPFD_RAW_PF 1
