@@ -321,6 +321,13 @@ def test_nccl_transport_single_rank(b200):
             assert same_bits(ref.get_field(cls, comp), nc.get_field(cls, comp))
     assert [(x.kinetic_energy, x.enstrophy) for x in r1.series] == \
            [(x.kinetic_energy, x.enstrophy) for x in r2.series]
+    # measured halo volume (mpfd_b200_halo_bytes): every exchange is two
+    # ncclSend messages of 4 ghost planes x 5 components in q storage (fp32
+    # in HPSP); at least one exchange per substep (4 steps x 3 substeps)
+    blk = 4 * 5 * n * n * 4
+    sent = nc.halo_bytes()
+    assert sent % (2 * blk) == 0 and sent >= 2 * blk * 4 * 3
+    assert ref.halo_bytes() == 0
     # divergence through the NCCL reduction of the event record
     kw = dict(preset="DP", split="Divergence", viscous=False, mach=0.4)
     a = b200_solver(b200, 16, **kw)
@@ -338,8 +345,7 @@ def test_nccl_transport_single_rank(b200):
 @pytest.mark.parametrize("preset", ["DP", "SPDP", "HPSP"])
 def test_full_size_paths_agree(b200, preset):
     """BASELINE.json's 512^3 workload, one RK step: the fused kernel the bench
-    times (warp-specialised for HPSP, packed fp32 pairs for SPDP, scalar fp64
-    for DP) and the staged one-kernel-per-level path -- two independent
+    times (warp-specialised for HPSP and SPDP, scalar fp64 for DP) and the staged one-kernel-per-level path -- two independent
     kernel implementations, each pinned bit for bit to the reference at small
     sizes -- leave bitwise identical Q and Qt at full size; the state stays
     finite and the density positive (a size-independent property check)."""
