@@ -491,6 +491,19 @@ struct KT<2> {
     using type = double;
 };
 
+// the dynamic shared-memory opt-in is a per-device function attribute: set it
+// once per (kernel, device) -- slabs may live on several devices (LOCAL mode)
+template <class K>
+static void smem_optin(K kern, size_t smem, unsigned& done_mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned bit = 1u << (dev & 31);
+    if (!(done_mask & bit)) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        done_mask |= bit;
+    }
+}
+
 template <int MODE, int QK, int TK, int RK, int WK>
 struct FusedPlan {
     static constexpr bool available = true;
@@ -584,9 +597,10 @@ struct FusedPlan {
             if (a.g.nx % 2 == 0) {
                 auto kern = k_fused_ws<QS, TS, RS, PT, WC, T, TC, QC, ST, TLW, NPW, SPL>;
                 constexpr size_t smem = WsSmem<TLW, T, PT, QS>::total;
+                static unsigned done = 0;
                 static int ok = -1;
+                smem_optin(kern, smem, done);
                 if (ok < 0) {
-                    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                     cudaFuncAttributes fa{};
                     ok = cudaFuncGetAttributes(&fa, kern) == cudaSuccess && WsRegs<T, TLW, NPW>::fits(fa.numRegs);
                 }
@@ -602,11 +616,8 @@ struct FusedPlan {
             if (a.g.nx % 2 == 0) {
             auto kern = k_fused2<QS, TS, RS, PT, WC, T, TC, QC, ST, TL2, MINB2, SPL, STAGE2>;
             constexpr size_t smem = SMEM2;
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                attr = true;
-            }
+            static unsigned done = 0;
+            smem_optin(kern, smem, done);
             a.lz = z_range(a.g, a.zhi - a.zlo, TL2::TX, TL2::TY, MINB2);
             const dim3 grid((a.g.nx + TL2::TX - 1) / TL2::TX, (a.g.ny + TL2::TY - 1) / TL2::TY,
                             (a.zhi - a.zlo + a.lz - 1) / a.lz);
@@ -616,11 +627,8 @@ struct FusedPlan {
         }
         auto kern = k_fused<QS, TS, RS, PT, WC, T, TC, QC, ST, TL, FT::MINB, SPL, FT::STAGE>;
         constexpr size_t smem = FT::SMEM;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
+        static unsigned done = 0;
+        smem_optin(kern, smem, done);
         a.lz = z_range(a.g, a.zhi - a.zlo, TL::TX, TL::TY, FT::MINB);
         const dim3 grid((a.g.nx + TL::TX - 1) / TL::TX, (a.g.ny + TL::TY - 1) / TL::TY,
                         (a.zhi - a.zlo + a.lz - 1) / a.lz);
