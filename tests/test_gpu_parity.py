@@ -206,7 +206,7 @@ def test_local_slabs_bitwise(b200, pz):
 
 
 @pytest.mark.parametrize("pz", [2, 3, 4])
-@pytest.mark.parametrize("preset", ["DP", "HPSP"])
+@pytest.mark.parametrize("preset", ["DP", "SPDP", "HPSP"])
 def test_overlapped_exchange_bitwise(b200, preset, pz):
     """Interior launch overlapped with the ghost-plane exchange, boundary
     launches after it: bitwise equal to the exchange-first schedule and to
