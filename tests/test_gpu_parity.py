@@ -363,3 +363,26 @@ def test_full_size_paths_agree(b200, preset):
         assert same_bits(a, b), f"{preset} 512^3 class {i // 5} comp {i % 5}"
     rho = out["fused"][0]
     assert np.isfinite(rho).all() and (rho > 0).all()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("preset", ["DP", "SPDP", "HPSP"])
+def test_history_64(b200, preset):
+    """KE / enstrophy history contract: TGV 64^3,
+    M=0.1, Re=1600, dt=0.002, t in [0, 0.5] sampled every 25 steps, against
+    the reference -- bit for bit (the states are bitwise equal and the
+    reduction tree is the reference's), far inside the stated tolerance
+    (max rel dK, d enstrophy <= 1e-12); the fused kernels the bench times."""
+    n, dt, steps, every = 64, 0.002, 250, 25
+    s = b200_solver(b200, n, preset)
+    c = checker(n, preset=preset, threads=8) if po.ref_available() else checker(n, preset=preset)
+    s.init_tgv()
+    c.init()
+    r = s.advance(b200.StepConfig(dt, steps, every), threads=8)
+    st, series, _, it = c.advance(dt, steps, every, threads=8)
+    assert not r.diverged and st == 0 and r.iterations_run == it == steps
+    got = np.array([[x.t, x.kinetic_energy, x.enstrophy, x.eps_s] for x in r.series])
+    assert got.shape == (steps // every + 1, 4)
+    assert same_bits(got, series[:, :4])
+    rel = np.abs(got[:, 1:3] - series[:, 1:3]) / np.abs(series[:, 1:3])
+    assert rel.max() <= 1e-12
