@@ -42,6 +42,11 @@ extern "C" int probe_prim_f64(const double* in, long n, double* fast, double* re
                               double gM2) {
     return run<double>(in, n, fast, ref, half, gm1, gM2);
 }
+// in: n pairs x 5 float2 (lane pairs), bit patterns
+extern "C" int probe_prim_f2(const float* in, long n, float* fast, float* ref, double half, double gm1, double gM2) {
+    return run<float2>(in, n, fast, ref, make_float2((float)half, (float)half), make_float2((float)gm1, (float)gm1),
+                       make_float2((float)gM2, (float)gM2));
+}
 // in: n pairs x 5 half2 words (lane pairs), bit patterns
 extern "C" int probe_prim_h2(const unsigned* in, long n, unsigned* fast, unsigned* ref, double half, double gm1,
                              double gM2) {
