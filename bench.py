@@ -158,9 +158,10 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": None, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": dtype_of(args.precision), "data": "synthetic",
-        "config": {"workload": f"TGV {args.grid}^3 {args.precision}", "sample": sample},
+        "config": {"workload": f"TGV {args.grid}^3 {args.precision}", "n": args.grid,
+                   "precision": args.precision, "sample": sample},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
