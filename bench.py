@@ -111,24 +111,15 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def cpu_reference_run(preset, strategy, emulation, steps, warmup, threads=None, n=None,
-                      budget_s=20.0):
-    """Time the reference CPU implementation (oracle/_ref, else the C port) on
-    this host on a bounded sample grid; returns (pt/s, cores, kind, sample)."""
+def cpu_reference_run(preset, strategy, emulation, n, steps, warmup, threads=None):
+    """Time the reference CPU implementation (oracle/_ref: the unmodified
+    reference sources, else the C port) through its advance() on this host's
+    cores, on the n^3 TGV grid itself; returns (pt/s, cores, kind, sample)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
 
     threads = threads or os.cpu_count() or 1
     kind = "reference" if po.ref_available() else "port"
-    # sample size: the per-point rate is grid-size independent on CPU; pick
-    # the largest of 48..128 whose step fits the budget (HPSP Strict ~8x DP)
-    slow = 8.0 if (emulation == "strict" and PRESET_KINDS[preset][2] == 2) else 1.0
-    est_rate = 2.0e6 * max(1, threads) / 8.0 / slow  # pt/s, SURVEY 6 (8 threads: ~2 Mpt/s DP)
-    if n is None:
-        n = 48
-        for cand in (64, 80, 96, 128):
-            if cand ** 3 / est_rate * (steps + warmup) <= budget_s:
-                n = cand
     kw = dict(preset=preset, strategy=strategy, emulation=emulation)
     if kind == "reference":
         c = po.Reference(n, threads=threads, **kw)
@@ -142,32 +133,63 @@ def cpu_reference_run(preset, strategy, emulation, steps, warmup, threads=None, 
     t0 = time.perf_counter()
     c.advance(dt, steps, 0, threads=threads)
     el = time.perf_counter() - t0
+    del c
     rate = n ** 3 * steps / el
-    sample = (f"TGV {n}^3 {preset} {strategy} {emulation}, {steps} RK steps after {warmup} "
+    sample = (f"TGV {n}^3 {preset} {strategy} {emulation}, {steps} timed RK step(s) after {warmup} "
               f"warm-up, {'reference advance() (oracle/_ref)' if kind == 'reference' else 'C port (oracle/)'}, "
-              f"threads={threads}")
+              f"threads={threads}, {el / steps:.2f} s/step")
     return rate, threads, kind, sample
+
+
+# CPU steps are ~1e4x slower than the GPU's: the reference runs the bench's
+# own grid for a bounded number of steps (1 warm-up + 2 timed)
+CPU_STEPS, CPU_WARMUP = 2, 1
+# per-precision CPU lines run at 256^3, one timed step (HPSP Strict emulates
+# binary16 in software: ~8x a DP step on the CPU)
+CPU_PP_GRID = 256
+
+
+def cpu_per_precision(modes, args):
+    out = {}
+    for p in modes:
+        try:
+            rate, cores, kind, sample = cpu_reference_run(p, args.strategy, args.emulation,
+                                                          min(args.grid, CPU_PP_GRID), 1, 0)
+            out[p] = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+        except Exception as e:  # report, never hide
+            out[p] = {"value": None, "error": str(e)}
+    return out
 
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    steps, warmup = min(args.steps, CPU_STEPS), min(args.warmup, CPU_WARMUP)
     rate, cores, kind, sample = cpu_reference_run(args.precision, args.strategy, args.emulation,
-                                                  args.steps, args.warmup)
+                                                  args.grid, steps, warmup)
+    bound = (f"{steps} timed + {warmup} warm-up step(s) of the {args.grid}^3 grid instead of "
+             f"{args.steps} + {args.warmup}: a CPU step of this grid takes tens of seconds")
+    modes = [x for x in args.modes.split(",") if x and x != args.precision]
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": args.scaling,
+        "ms_per_step": n_ms(rate, args.grid), "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": dtype_of(args.precision), "data": "synthetic",
-        "config": {"workload": f"TGV {args.grid}^3 {args.precision}", "n": args.grid,
-                   "precision": args.precision, "sample": sample},
+        "config": {"workload": f"TGV {args.grid}^3 {args.precision} (M=0.1, Re=1600, {args.split}, "
+                               f"{args.strategy}, {args.emulation})",
+                   "n": args.grid, "precision": args.precision, "sample": sample, "bounded": bound},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "per_precision": cpu_per_precision(modes, args),
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def n_ms(rate, n):
+    return n ** 3 / rate * 1e3 if rate else None
 
 
 def dtype_of(preset):
@@ -219,6 +241,10 @@ def main():
                               MASTER_PORT=os.environ.get("MASTER_PORT", "29533"))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     hbm, peak_src = peaks()
+    try:
+        ceil = m.issue_ceiling(local)
+    except Exception as e:  # report, never hide
+        ceil = {"error": str(e)}
 
     def measure(preset, with_extras):
         n = args.grid
@@ -269,16 +295,21 @@ def main():
         nloc = npts // world
         fused = klaunch[1] == 0
         if fused:
-            # compulsory per substep: read Q, write Q; Qt read (substeps 1,2) + write
-            per_pt = (10 * bq + 5 * bt) / 3 + 2 * (10 * bq + 10 * bt) / 3
+            # the kernel's own compulsory bytes per substep: read Q, write Q;
+            # Qt read (substeps 1,2) + write
+            comp_pt = (10 * bq + 5 * bt) / 3 + 2 * (10 * bq + 10 * bt) / 3
             kname = "fused residual + RK stage update"
         else:
-            per_pt = 5 * bq + 5 * br
+            comp_pt = 5 * bq + 5 * br
             kname = "staged residual (k_resid)"
         # dominant-kernel time per substep (an overlapped substep is one
         # interior + two boundary launches covering the slab once)
         avg_ms = kms[0] / (3 * args.steps) if fused else kms[0] / max(1, klaunch[0])
-        achieved = per_pt * nloc / (avg_ms * 1e-3) / 1e9
+        # achieved = SURVEY 8(d)'s algorithmic bytes (B_alg per point per RK
+        # step / 3 per substep launch) x the points one launch updates / the
+        # CUDA-event launch time
+        alg_pt = b_alg(preset) / 3
+        achieved = alg_pt * nloc / (avg_ms * 1e-3) / 1e9
         res = {
             "preset": preset, "value": rate, "ms_per_step": ms_step,
             "b_alg_bytes_per_pt": b_alg(preset),
@@ -286,7 +317,13 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic_lookup(preset, nloc, fused),
                          "kernel": kname, "avg_ms_per_substep": avg_ms,
-                         "bytes_per_pt_per_launch": per_pt, "peak_source": peak_src},
+                         "basis": "B_alg/3 bytes per point per launch (SURVEY.md 8(d)); traffic = "
+                                  "ncu dram bytes of the same launch (profiles/ncu_traffic.json)",
+                         "bytes_per_pt_per_launch": alg_pt,
+                         "compulsory_bytes_per_pt_per_launch": comp_pt,
+                         "compulsory_frac": comp_pt * nloc / (avg_ms * 1e-3) / 1e9 / hbm,
+                         "compute": compute_roofline(preset, nloc, avg_ms, ceil),
+                         "peak_source": peak_src},
             "kernel_ms": {"dominant": kms[0], "rk": kms[1], "halo": kms[2], "other": kms[3]},
             "gpu_launches": int(klaunch[0] + klaunch[1] + klaunch[3]),
             "clocks": clk.summary(),
@@ -295,13 +332,16 @@ def main():
         if with_extras and not args.no_e2e:
             res["e2e"] = (e2e_run_slab(m, s, n, dt, args.steps, world, rank, zper) if use_nccl
                           else e2e_run(m, s, n, dt, args.steps, world, rank))
-        dev, census, census64 = s.memory()
+        mc = s.memory_census()
         bq_ = PRESET_KINDS[preset][0]
         res["memory"] = {
-            "device_bytes": dev, "census_bytes": census, "census_b64_bytes": census64,
-            "census_gain": census64 / census if census else None,
-            "note": "device_bytes: HBM this solver holds (Q, Qt double-buffered, R); census: the "
-                    "reference's analytic memory_report of its field set (registry.cpp:24-39)"}
+            "device_bytes": mc["device_bytes"], "census_bytes": mc["total_bytes"],
+            "census_b64_bytes": mc["baseline_b64_bytes"], "census_gain": mc["gain"],
+            "device_gain_vs_census_b64": mc["baseline_b64_bytes"] / mc["device_bytes"],
+            "census_per_class": mc["per_class"],
+            "note": "device_bytes: HBM this solver holds (Q double-buffered, Qt in place, R never "
+                    "allocated on the fused path); census: the reference's analytic memory_report "
+                    "of its field set (registry.cpp:24-39)"}
         if use_nccl:
             # measured ncclSend bytes per RK step vs comm_volume_report's model
             # (registry.cpp:41-66; depth 2, q exchanged 3x per iteration)
@@ -320,8 +360,9 @@ def main():
     for p in [x for x in args.modes.split(",") if x and x != args.precision]:
         try:
             r = measure(p, False)
-            extra[p] = {k: r[k] for k in ("value", "ms_per_step", "b_alg_frac", "path")}
+            extra[p] = {k: r[k] for k in ("value", "ms_per_step", "b_alg_frac", "path", "memory")}
             extra[p]["roofline_frac"] = r["roofline"]["frac"]
+            extra[p]["compute"] = r["roofline"]["compute"]
         except Exception as e:  # report, never hide
             extra[p] = {"error": str(e)}
 
@@ -352,7 +393,9 @@ def main():
             "kernel_ms": head["kernel_ms"],
             "per_precision": {args.precision: {"value": head["value"],
                                                "ms_per_step": head["ms_per_step"],
-                                               "b_alg_frac": head["b_alg_frac"]}, **extra},
+                                               "b_alg_frac": head["b_alg_frac"],
+                                               "memory": head.get("memory")}, **extra},
+            "issue_ceiling_lane_ops_per_s": ceil,
         }
         if "e2e" in head:
             line["e2e"] = head["e2e"]
@@ -361,15 +404,50 @@ def main():
         if not args.no_cpu_baseline and world == 1:
             try:
                 rate, cores, kind, sample = cpu_reference_run(args.precision, args.strategy,
-                                                              args.emulation, 2, 1)
+                                                              args.emulation, args.grid,
+                                                              CPU_STEPS, CPU_WARMUP)
                 line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores,
                                         "kind": kind, "sample": sample}
             except Exception as e:
                 line["cpu_baseline"] = {"value": None, "error": str(e)}
+            for p, v in cpu_per_precision([p for p in extra if "error" not in extra[p]], args).items():
+                extra[p]["cpu_baseline"] = v
         print(json.dumps(line), flush=True)
     if use_nccl:
         dist.destroy_process_group()
     return 0
+
+
+PIPE = {8: "fp64 (DADD/DMUL)", 4: "fp32 pairs (FADD2/FFMA2)", 2: "fp16 pairs (HADD2/HMUL2)"}
+CEIL_KEY = {8: "fp64", 4: "fp32", 2: "fp16"}
+
+
+def compute_roofline(preset, npts, avg_ms, ceil):
+    """Secondary (compute) roofline of the fused kernel: its floating-point
+    lane operations per point per launch, counted by ncu on the committed
+    capture (profiles/ncu_ops.json: smsp__sass_thread_inst_executed_op_*
+    summed over the residual compute type's add/mul/fma, packed
+    instructions counted per lane), at the CUDA-event launch time, against
+    the measured issue ceiling of that arithmetic (mpfd_b200_issue_ceiling)."""
+    rb = PRESET_KINDS[preset][2]
+    out = {"pipe": PIPE[rb], "ceiling_gops": None, "ops_per_pt_per_launch": None,
+           "achieved_gops": None, "frac": None}
+    if isinstance(ceil, dict) and CEIL_KEY[rb] in ceil:
+        out["ceiling_gops"] = ceil[CEIL_KEY[rb]] / 1e9
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_ops.json")) as f:
+            d = json.load(f)
+        ops = d.get(f"{preset}/fused/ops_per_pt")
+        pct = d.get(f"{preset}/fused/pipe_active_pct")
+    except Exception:
+        ops = pct = None
+    if ops:
+        out["ops_per_pt_per_launch"] = ops
+        out["achieved_gops"] = ops * npts / (avg_ms * 1e-3) / 1e9
+        if out["ceiling_gops"]:
+            out["frac"] = out["achieved_gops"] / out["ceiling_gops"]
+    out["ncu_pipe_active_pct"] = pct
+    return out
 
 
 def traffic_lookup(preset, npts, fused):

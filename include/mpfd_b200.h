@@ -172,6 +172,42 @@ int mpfd_b200_diagnostics(mpfd_solver* s, int weighting, double t, int threads, 
 int mpfd_b200_advance(mpfd_solver* s, const mpfd_step* step, mpfd_diag* series, long cap,
                       long* len, mpfd_divergence* ev, long* iters);
 
+/* AdvanceResult's timing (integrate.hpp:35-43, integrate.cpp:102, 162-165)
+ * of the last mpfd_b200_advance call: wall seconds around the whole call
+ * (samples and snapshots included, as in the reference) and seconds per
+ * completed iteration. */
+typedef struct {
+    long iterations_run;
+    double wall_seconds;
+    double seconds_per_iteration;
+} mpfd_advance_info;
+int mpfd_b200_advance_info(mpfd_solver* s, mpfd_advance_info* out);
+
+/* MemoryReport (registry.hpp:40-45) of the reference's field set for this
+ * solver's precision config and strategy (memory_report over
+ * make_solver_fields, registry.cpp:24-39, physics.cpp:441-475), indexed by
+ * ArrayClass (q_vector, rk_arrays, residuals, wk_arrays, diagnostics), plus
+ * the HBM this solver actually holds (device_bytes). */
+typedef struct {
+    long count[5];
+    size_t bytes[5];
+    size_t total_bytes;
+    size_t baseline_b64_bytes;
+    double gain;
+    size_t device_bytes;
+} mpfd_memory_census;
+int mpfd_b200_memory_census(mpfd_solver* s, mpfd_memory_census* out);
+
+/* Exact divergence state (default off).  On: Qt and R are double-buffered,
+ * every substep writes R, and every slab / rank finishes a substep before any
+ * starts the next, so Q, Qt and R at a divergence event are the reference's
+ * bit for bit.  Off (the lean layout): Qt is updated in place and R is
+ * computed on demand from the double-buffered Q; Q and the event are still
+ * exact, Qt is exact for a nonfinite-state event, R for nonfinite-state and
+ * nonfinite-residual events, and with several slabs the slabs that did not
+ * diverge may stand up to a few substeps later. */
+int mpfd_b200_set_exact_divergence(mpfd_solver* s, int enable);
+
 /* write_snapshot (io.cpp:69-85): int32 {n, n, n, 5} then the five conserved
  * components as binary64 n^3 arrays (i fastest).  Whole state in this
  * process only (one slab or LOCAL slabs, z_periods 1). */
@@ -214,6 +250,12 @@ int mpfd_b200_field_kind(const mpfd_precision* prec, int cls, const char* name, 
 /* Bytes this rank has handed to ncclSend for halo exchanges since creation
  * (the measured counterpart of comm_volume_report, registry.cpp:41-66). */
 int mpfd_b200_halo_bytes(mpfd_solver* s, unsigned long long* sent);
+
+/* Measured issue ceilings of the residual's arithmetic on `device` (SURVEY.md
+ * 7 hard part 1), lane operations per second of unfused add/mul in the forms
+ * the kernels emit: out[0] fp64 (DADD/DMUL), out[1] fp32 pairs (FADD2 /
+ * FFMA2 with an opaque zero), out[2] fp16 pairs (HADD2/HMUL2). */
+int mpfd_b200_issue_ceiling(int device, double out[3]);
 
 /* Which residual path runs: 0 = staged multi-kernel, 1 = fused. */
 int mpfd_b200_set_path(mpfd_solver* s, int path);

@@ -56,6 +56,8 @@ struct AdvanceResult {
     bool diverged = false;
     std::optional<DivergenceEvent> divergence;
     long iterations_run = 0;
+    double wall_seconds = 0.0;           // integrate.hpp:41-42
+    double seconds_per_iteration = 0.0;
     std::vector<mpfd_diag> series;
 };
 
@@ -117,6 +119,10 @@ class Solver {
         mpfd_divergence d{};
         const int rc = check(mpfd_b200_advance(s_, &step, r.series.data(), cap, &len, &d, &r.iterations_run));
         r.series.resize((size_t)len);
+        mpfd_advance_info info{};
+        check(mpfd_b200_advance_info(s_, &info));
+        r.wall_seconds = info.wall_seconds;
+        r.seconds_per_iteration = info.seconds_per_iteration;
         if (rc == MPFD_DIVERGED) {
             r.diverged = true;
             r.divergence = to_event(d);
@@ -129,6 +135,16 @@ class Solver {
     void set_snapshots(const std::vector<double>& times, const char* path) {
         check(mpfd_b200_set_snapshots(s_, times.data(), (int)times.size(), path));
     }
+
+    // memory_report of the reference's field set (registry.cpp:24-39) + the
+    // HBM this solver holds
+    mpfd_memory_census memory_census() const {
+        mpfd_memory_census m{};
+        check(mpfd_b200_memory_census(s_, &m));
+        return m;
+    }
+    // exact divergence state (Qt, R double-buffered; see mpfd_b200.h)
+    void set_exact_divergence(bool on) { check(mpfd_b200_set_exact_divergence(s_, on ? 1 : 0)); }
 
     mpfd_solver* handle() const { return s_; }
 

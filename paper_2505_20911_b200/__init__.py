@@ -12,7 +12,7 @@ from .solver import (  # noqa: F401
     B16, B32, B64, DEFAULT, STORESOME, STRICT, STOREROUND,
     ConfigError, DeviceError, DivergenceEvent, DiagnosticsRecord, AdvanceResult,
     FlowParams, GridSpec, PrecisionConfig, RKScheme, SplitCoefficients, StepConfig,
-    Decomposition, Solver, lib, resolve_preset, split_preset, library_path,
+    Decomposition, Solver, lib, resolve_preset, split_preset, library_path, issue_ceiling,
 )
 
 __all__ = [
@@ -20,5 +20,5 @@ __all__ = [
     "ConfigError", "DeviceError", "DivergenceEvent", "DiagnosticsRecord", "AdvanceResult",
     "FlowParams", "GridSpec", "PrecisionConfig", "RKScheme", "SplitCoefficients",
     "StepConfig", "Decomposition", "Solver", "lib", "resolve_preset", "split_preset",
-    "library_path",
+    "library_path", "issue_ceiling",
 ]

@@ -62,7 +62,7 @@ struct FusedArgs {
     ResConsts rc;
     StageConsts sc;
     RkConsts kc;
-    int write_r;
+    int write_r;   // 0: Q, Qt; 1: Q, Qt and R; 2: R only
     int lz;        // z planes per CTA
     int zlo, zhi;  // local output planes [zlo, zhi) of this launch
     DevDiv* div;
@@ -208,10 +208,12 @@ __device__ __forceinline__ void rk_point(const FusedArgs& a, int comp, int c, lo
     const TC t = Op<TC>::mul(dt_c, cvt<TC>(rs));
     const TC v = a.kc.skip_a ? t : Op<TC>::add(Op<TC>::mul(a_c, cvt<TC>(in.qt)), t);
     const TS vs = cvt<TS>(v);
-    ((TS*)a.qtout)[ir] = vs;
     const QC nq = Op<QC>::add(cvt<QC>(in.q), Op<QC>::mul(b_c, cvt<QC>(vs)));
     const QS ns = cvt<QS>(nq);
-    ((QS*)a.qout)[iq] = ns;
+    if (a.write_r != 2) {  // 2: residual only (Solver::materialize_r)
+        ((TS*)a.qtout)[ir] = vs;
+        ((QS*)a.qout)[iq] = ns;
+    }
     if (a.write_r) ((RS*)a.r)[ir] = rs;
     if (nonfinite(rs) | nonfinite(ns)) {
         const unsigned long long gi = ((unsigned long long)(g.z0 + c) * g.ny + y) * g.nx + x;
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
     // a substep after a divergence is a no-op; launches of the substep that
     // diverged (interior and boundary of an overlapped substep) all run, so
     // the first point in scan order is found
-    if (a.div->flag && (a.div->iter != a.iter || a.div->sub != a.sub)) return;
+    if (a.div->key < div_key(a.iter, a.sub)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using SM = FusedSmem<TL, T, PT>;
     PT* Pr = (PT*)smem_raw;

@@ -115,10 +115,12 @@ __device__ __forceinline__ void rk_pair(const FusedArgs& a, int comp, int c, lon
     const TC2 t = Op<TC2>::mul(dt_c, cvt<TC2>(rs));
     const TC2 v = a.kc.skip_a ? t : Op<TC2>::add(Op<TC2>::mul(a_c, cvt<TC2>(in.qt)), t);
     const TS2 vs = cvt<TS2>(v);
-    stv<TS>((TS*)a.qtout + ir, vs);
     const QC2 nq = Op<QC2>::add(cvt<QC2>(in.q), Op<QC2>::mul(b_c, cvt<QC2>(vs)));
     const QS2 ns = cvt<QS2>(nq);
-    stv<QS>((QS*)a.qout + iq, ns);
+    if (a.write_r != 2) {  // 2: residual only (Solver::materialize_r)
+        stv<TS>((TS*)a.qtout + ir, vs);
+        stv<QS>((QS*)a.qout + iq, ns);
+    }
     if (a.write_r) stv<RS>((RS*)a.r + ir, rs);
     if (nonfinite2(rs) | nonfinite2(ns)) {
         const unsigned bits = (nonfinite(lo(rs)) ? 1u : 0u) | (nonfinite(hi(rs)) ? 2u : 0u) |
@@ -145,7 +147,7 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
     // a substep after a divergence is a no-op; launches of the substep that
     // diverged (interior and boundary of an overlapped substep) all run, so
     // the first point in scan order is found
-    if (a.div->flag && (a.div->iter != a.iter || a.div->sub != a.sub)) return;
+    if (a.div->key < div_key(a.iter, a.sub)) return;
     using T2 = typename V2<T>::type;
     using WC2 = typename V2<WC>::type;
     using PT2 = typename V2<PT>::type;
@@ -637,7 +639,7 @@ struct FusedPlan {
 
     static void launch(const Geo& g, cudaStream_t st, const void* qin, void* qout, const void* qtin, void* qtout,
                        void* r, const PrimConsts& pc, const ResConsts& rc, const StageConsts& sc, bool staged,
-                       const RkConsts& kc, bool write_r, DevDiv* div, int iter, int sub, int zlo, int zhi) {
+                       const RkConsts& kc, int write_r, DevDiv* div, int iter, int sub, int zlo, int zhi) {
         FusedArgs a;
         using KT_ = KBits<T>;
         a.kb[K_R] = KT_::of(rc.r);
@@ -666,7 +668,7 @@ struct FusedPlan {
         a.rc = rc;
         a.sc = sc;
         a.kc = kc;
-        a.write_r = write_r ? 1 : 0;
+        a.write_r = write_r;
         a.div = div;
         a.iter = iter;
         a.sub = sub;

@@ -30,21 +30,27 @@ struct Geo {
     int planes;       // nzl + 2*kHalo
 };
 
-// divergence record, first-in-scan-order per (code, component) via atomicMin
+// divergence record.  Every entry carries its substep key (iteration * 3 +
+// substep) above the global scan-order index, so one atomicMin keeps the
+// earliest substep first and, inside it, the first point in scan order
+// (reduce.cpp:57-81, physics.cpp:309-312, integrate.cpp:135-147); merging
+// slabs or ranks is a plain minimum.  key: the smallest substep key recorded
+// (ULLONG_MAX: none) -- launches of a later substep are no-ops.
+constexpr int kDivKeyShift = 39;  // global index < 2^39 points, key < 2^25
 struct DevDiv {
-    int flag;
-    int iter;
-    int sub;
-    int pad;
+    unsigned long long key;
     unsigned long long idx[3][5];
 };
 
+__host__ __device__ __forceinline__ unsigned long long div_key(long long iter, int sub) {
+    return (unsigned long long)iter * 3ull + (unsigned long long)sub;
+}
+
 __device__ __forceinline__ void record_div(DevDiv* d, int code, int comp, unsigned long long gidx,
                                            int iter, int sub) {
-    atomicMin(&d->idx[code][comp], gidx);
-    d->iter = iter;
-    d->sub = sub;
-    atomicOr(&d->flag, 1);
+    const unsigned long long key = div_key(iter, sub);
+    atomicMin(&d->idx[code][comp], (key << kDivKeyShift) | gidx);
+    atomicMin(&d->key, key);
 }
 
 __device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
@@ -122,7 +128,7 @@ struct PrimConsts {
 template <class QS, class WC, class PT>
 __global__ void __launch_bounds__(256) k_prim(Geo g, const QS* __restrict__ q, PT* __restrict__ prim,
                                               PrimConsts pc, DevDiv* div, int iter, int sub) {
-    if (div->flag) return;
+    if (div->key != ~0ull) return;
     using O = Op<WC>;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -168,7 +174,7 @@ struct StageConsts {
 template <class T, class WC, class PT, bool STAGED>
 __global__ void __launch_bounds__(256) k_level2(Geo g, const PT* __restrict__ prim, T* __restrict__ lev2,
                                                 ResConsts rc_, StageConsts sc, DevDiv* div) {
-    if (div->flag) return;
+    if (div->key != ~0ull) return;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     const int p = blockIdx.z + kHalo - 2;
@@ -220,7 +226,7 @@ template <class T, class QS, class PT, class RS>
 __global__ void __launch_bounds__(256) k_resid(Geo g, const QS* __restrict__ q, const PT* __restrict__ prim,
                                                const T* __restrict__ lev2, RS* __restrict__ r,
                                                ResConsts rc_, DevDiv* div, int iter, int sub) {
-    if (div->flag) return;
+    if (div->key != ~0ull) return;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     const int z = blockIdx.z;
@@ -254,7 +260,7 @@ template <class QS, class TS, class RS, class TC, class QC>
 __global__ void __launch_bounds__(256) k_rk(Geo g, QS* __restrict__ q, TS* __restrict__ qt,
                                             const RS* __restrict__ r, RkConsts kc, DevDiv* div, int iter,
                                             int sub) {
-    if (div->flag) return;
+    if (div->key != ~0ull) return;
     const long long n = (long long)g.nzl * g.plane;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -286,12 +292,8 @@ __global__ void __launch_bounds__(256) k_rk(Geo g, QS* __restrict__ q, TS* __res
 // integrand: which = 0 kinetic energy (plain / density weighted),
 // which = 1 |curl u|^2 with the binary64 d1 stencil (r = 1/(12h) uncvt'd)
 template <class QS>
-__global__ void __launch_bounds__(256) k_diag_integrand(Geo g, const QS* __restrict__ q, double* __restrict__ out,
-                                                        int which, int density, double r) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    const int z = blockIdx.z;
-    if (x >= g.nx || y >= g.ny) return;
+__device__ __forceinline__ double diag_point(const Geo& g, const QS* __restrict__ q, int x, int y, int z,
+                                             int which, int density, double r) {
     const long long o = (long long)y * g.nx + x;
     double val;
     if (which == 0) {
@@ -321,29 +323,56 @@ __global__ void __launch_bounds__(256) k_diag_integrand(Geo g, const QS* __restr
         const double wz = __dsub_rn(D1(1, 0), D1(0, 1));
         val = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz));
     }
-    out[(long long)z * g.plane + o] = val;
+    return val;
 }
 
-// pairwise_sum of 4096-element chunks (reduce.cpp:14-22): 128 sequential
-// leaves of 32, then a perfect binary tree.  One warp per chunk: each lane
-// owns 4 consecutive leaves, the lane tree is a xor butterfly (IEEE addition
-// is commutative, so both partners hold the same bits).
-static __global__ void k_chunk_sums(const double* __restrict__ v, long long nchunks, double* __restrict__ out) {
-    const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (w >= nchunks) return;
-    const double* base = v + w * 4096 + lane * 128;
-    double leaf[4];
-#pragma unroll
-    for (int l = 0; l < 4; ++l) {
+// the whole integrand in HBM (small / unaligned grids only: the host then
+// runs the reference's tree over it)
+template <class QS>
+__global__ void __launch_bounds__(256) k_diag_integrand(Geo g, const QS* __restrict__ q, double* __restrict__ out,
+                                                        int which, int density, double r) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int z = blockIdx.z;
+    if (x >= g.nx || y >= g.ny) return;
+    out[(long long)z * g.plane + (long long)y * g.nx + x] = diag_point<QS>(g, q, x, y, z, which, density, r);
+}
+
+// integrand fused with deterministic_sum's 4096-element chunk sums
+// (reduce.cpp:14-36): no n^3 integrand buffer.  One 128-thread CTA per chunk
+// (grid-stride): the chunk's 4096 integrand values are computed coalesced
+// into shared memory (one pad word per 32 so the leaf reads are conflict
+// free), thread L sums leaf L (elements 32L..32L+31) sequentially from 0.0 as
+// pairwise_sum does for n <= 32, and the 128 leaves meet in the perfect
+// binary tree: a xor butterfly inside each warp (IEEE addition commutes, so
+// both partners hold the same bits), then (w0 + w1) + (w2 + w3).
+template <class QS>
+__global__ void __launch_bounds__(128) k_diag_chunks(Geo g, const QS* __restrict__ q, int which, int density,
+                                                     double r, long long nchunks, double* __restrict__ out) {
+    __shared__ double v[4096 + 128];
+    __shared__ double ws[4];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        const long long base = ch * 4096;
+        for (int k = 0; k < 32; ++k) {
+            const int e = tid + 128 * k;
+            const long long gi = base + e;
+            const int z = (int)(gi / g.plane);
+            const long long rem = gi - (long long)z * g.plane;
+            const int y = (int)(rem / g.nx), x = (int)(rem - (long long)y * g.nx);
+            v[e + (e >> 5)] = diag_point<QS>(g, q, x, y, z, which, density, r);
+        }
+        __syncthreads();
+        const double* lp = v + tid * 33;
         double s = 0.0;
-        for (int i = 0; i < 32; ++i) s = __dadd_rn(s, base[l * 32 + i]);
-        leaf[l] = s;
-    }
-    double acc = __dadd_rn(__dadd_rn(leaf[0], leaf[1]), __dadd_rn(leaf[2], leaf[3]));
+        for (int i = 0; i < 32; ++i) s = __dadd_rn(s, lp[i]);
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
-    if (lane == 0) out[w] = acc;
+        for (int off = 1; off < 32; off <<= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+        if (lane == 0) ws[warp] = s;
+        __syncthreads();
+        if (tid == 0) out[ch] = __dadd_rn(__dadd_rn(ws[0], ws[1]), __dadd_rn(ws[2], ws[3]));
+        __syncthreads();
+    }
 }
 
 }  // namespace mpfd_b200

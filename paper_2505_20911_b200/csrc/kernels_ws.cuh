@@ -104,7 +104,7 @@ struct WsRegs {
 template <class QS, class TS, class RS, class PT, class WC, class T, class TC, class QC, bool STAGED, class TL,
           int NPW, unsigned SPL>
 __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs a) {
-    if (a.div->flag && (a.div->iter != a.iter || a.div->sub != a.sub)) return;
+    if (a.div->key < div_key(a.iter, a.sub)) return;
     using T2 = typename V2<T>::type;
     using WC2 = typename V2<WC>::type;
     using PT2 = typename V2<PT>::type;

@@ -169,14 +169,29 @@ struct Solver {
     void* comm = nullptr;
     int path = 1;  // 1 fused when available, 0 staged
     bool halo_fresh = false;
-    int qbuf = 0;  // fused path: which Q/Qt buffer holds the state
+    int qbuf = 0;  // fused path: which Q buffer (and, exact mode, Qt buffer) holds the state
+    // Exact-divergence mode (off by default): Qt and R double-buffered, R
+    // written by every substep, and every slab / rank finishes a substep
+    // before any starts the next, so the state returned at a divergence event
+    // is the reference's exactly.  Default: Qt updated in place (it is read
+    // only at its own point), R computed on demand from the Q buffer that
+    // held the last residual's input (Q is double-buffered anyway).
+    bool exact = false;
+    int rbuf = 0;
+    enum { R_ZERO, R_MAT, R_PEND };
+    int r_state = R_ZERO;  // R_PEND: R = residual(Q buffer r_src), not yet computed
+    int r_src = 0;
+    bool r_alloc = false;
+    // wall time of the last advance (AdvanceResult, integrate.cpp:162-165)
+    double last_wall = 0.0, last_spi = 0.0;
+    long last_iters = 0;
     // timing
     bool profiling = false;
     double prof_ms[4] = {0, 0, 0, 0};
     long prof_launch[4] = {0, 0, 0, 0};
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[4];
     std::vector<cudaEvent_t> event_pool;
-    int* pinned_flag = nullptr;
+    unsigned long long* pinned = nullptr;  // 64 words: divergence keys / records, reductions
 
     ~Solver();
     void setup(const mpfd_grid* grid, const mpfd_precision* p, int strategy_, const mpfd_flow* flow,
@@ -188,7 +203,13 @@ struct Solver {
     bool fused_ok = false;  // fused kernels compiled for this plan and its wk overrides
     bool use_fused() const { return path == 1 && fused_ok; }
     void* qcur(const Slab& s) const { return (use_fused() && qbuf) ? s.q2 : s.q; }
-    void* qtcur(const Slab& s) const { return (use_fused() && qbuf) ? s.qt2 : s.qt; }
+    void* qbuf_ptr(const Slab& s, int b) const { return b ? s.q2 : s.q; }
+    void* qtcur(const Slab& s) const { return (use_fused() && exact && qbuf) ? s.qt2 : s.qt; }
+    void* rcur(const Slab& s) const { return (exact && rbuf) ? s.r2 : s.r; }
+    void ensure_r();
+    void materialize_r();
+    void set_exact(bool on);
+    void substep_barrier();
 
     // constants
     PrimConsts prim_consts() const;
@@ -200,6 +221,8 @@ struct Solver {
     void init(int case_kind);
     void set_interior(int cls, int comp, const double* src, size_t ld_row, size_t ld_plane, int off);
     void upload_slab(Slab& s, int cls, int comp, const double* src, size_t ld_row, size_t ld_plane);
+    void upload_planes(Slab& s, int cls, int comp, const double* src, size_t ld_row, size_t ld_plane, int zb,
+                       int nz);
     void get_interior(int cls, int comp, double* dst, size_t ld_row, size_t ld_plane, int off);
     void halo_refresh();
     // overlapped exchange (fused path): off for one slab per process with
@@ -211,7 +234,7 @@ struct Solver {
     void exchange_async();
     void residual_enqueue(int iter, int sub);
     void rk_enqueue(int sub, const double a[3], const double b[3], double dt, int iter);
-    void substep_enqueue(int sub, const double a[3], const double b[3], double dt, int iter, bool write_r);
+    void substep_enqueue(int sub, const double a[3], const double b[3], double dt, int iter);
     bool poll_div(bool block);
     bool resolve_div(mpfd_divergence* ev, double dt);
     void diagnostics(int weighting, double t, int threads, mpfd_diag* out);
@@ -225,22 +248,25 @@ struct Solver {
 Solver::~Solver() {
     for (auto& s : slabs) {
         cudaSetDevice(s.device);
-        for (void* p : {s.q, s.qt, s.r, s.q2, s.qt2, s.prim, s.lev2}) cudaFree(p);
+        for (void* p : {s.q, s.qt, s.r, s.q2, s.qt2, s.r2, s.prim, s.lev2}) cudaFree(p);
         cudaFree(s.diag);
         cudaFree(s.partials);
-        cudaFree(s.div);
+        cudaFree(s.gather);
+        cudaFree(s.red);
+        if (s.owns_div) cudaFree(s.div);
         cudaFree(s.staging);
         if (s.stream) cudaStreamDestroy(s.stream);
         if (s.comm) cudaStreamDestroy(s.comm);
         if (s.ev_x) cudaEventDestroy(s.ev_x);
         if (s.ev_b) cudaEventDestroy(s.ev_b);
+        if (s.ev_d) cudaEventDestroy(s.ev_d);
     }
     for (auto& v : prof_ev)
         for (auto& e : v) {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
         }
-    if (pinned_flag) cudaFreeHost(pinned_flag);
+    if (pinned) cudaFreeHost(pinned);
     if (comm) Nccl::get().commDestroy(comm);
 }
 
@@ -344,15 +370,15 @@ void Solver::setup(const mpfd_grid* grid, const mpfd_precision* p, int strategy_
 }
 
 void Solver::alloc() {
-    const size_t bq = byte_width(plan.qk), bt = byte_width(plan.tk), br = byte_width(plan.rk);
-    const size_t bp = byte_width(plan.pk);
-    const size_t bl = byte_width(plan.mode == 0 ? plan.rk : 2);
-    for (auto& s : slabs) {
+    const size_t bq = byte_width(plan.qk), bt = byte_width(plan.tk);
+    for (size_t i = 0; i < slabs.size(); ++i) {
+        Slab& s = slabs[i];
         CK(cudaSetDevice(s.device));
         CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&s.comm, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&s.ev_x, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&s.ev_b, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&s.ev_d, cudaEventDisableTiming));
         const size_t pl = (size_t)s.geo.plane;
         const size_t qel = (size_t)s.geo.planes * 5 * pl;
         const size_t iel = (size_t)s.geo.nzl * 5 * pl;
@@ -361,27 +387,148 @@ void Solver::alloc() {
             CK(cudaMemsetAsync(*p, 0, bytes, s.stream));
             s.bytes += bytes;
         };
+        // HBM-resident: Q (double-buffered on the fused path: neighbouring
+        // CTAs still read the old Q) and Qt (in place).  R is allocated on
+        // first use (ensure_r), the staged path's fields on first use
+        // (alloc_staged).
         get(&s.q, qel * bq);
         get(&s.qt, iel * bt);
-        get(&s.r, iel * br);
-        if (fused_ok) {
-            get(&s.q2, qel * bq);
-            get(&s.qt2, iel * bt);
+        if (fused_ok) get(&s.q2, qel * bq);
+        // LOCAL slabs on one device share one divergence record, so every
+        // slab's launches see the first event (a later substep is a no-op)
+        const Slab& s0 = slabs[0];
+        if (i > 0 && mode == MPFD_DECOMP_LOCAL && s.device == s0.device) {
+            s.div = s0.div;
+            s.owns_div = false;
+        } else {
+            CK(cudaMalloc(&s.div, sizeof(DevDiv)));
+            s.bytes += sizeof(DevDiv);
         }
-        CK(cudaMalloc(&s.div, sizeof(DevDiv)));
-        s.bytes += sizeof(DevDiv);
         const size_t nint = (size_t)s.geo.nzl * pl;
-        CK(cudaMalloc(&s.diag, nint * sizeof(double)));
-        CK(cudaMalloc(&s.partials, ((nint + 4095) / 4096) * sizeof(double)));
-        s.bytes += nint * sizeof(double) + ((nint + 4095) / 4096) * sizeof(double);
+        const size_t nch = (nint + 4095) / 4096;
+        CK(cudaMalloc(&s.partials, nch * sizeof(double)));
+        CK(cudaMalloc(&s.red, 16 * sizeof(unsigned long long)));
+        s.bytes += nch * sizeof(double) + 16 * sizeof(unsigned long long);
         s.staging_elems = std::min<size_t>(nint, (size_t)1 << 26);
         CK(cudaMalloc(&s.staging, s.staging_elems * sizeof(double)));
         s.bytes += s.staging_elems * sizeof(double);
     }
     if (!fused_ok) path = 0;
-    CK(cudaHostAlloc(&pinned_flag, sizeof(int) * 64, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&pinned, sizeof(unsigned long long) * 64, cudaHostAllocDefault));
     reset_div();
     sync();
+}
+
+// R on first use (make_solver_fields allocates it up front, physics.cpp:
+// 441-475; the fused path needs it only when R is read or written)
+void Solver::ensure_r() {
+    if (r_alloc) return;
+    const size_t br = byte_width(plan.rk);
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        const size_t bytes = (size_t)s.geo.nzl * 5 * s.geo.plane * br;
+        CK(cudaMalloc(&s.r, bytes));
+        CK(cudaMemsetAsync(s.r, 0, bytes, s.stream));
+        s.bytes += bytes;
+        if (exact) {
+            CK(cudaMalloc(&s.r2, bytes));
+            CK(cudaMemsetAsync(s.r2, 0, bytes, s.stream));
+            s.bytes += bytes;
+        }
+    }
+    r_alloc = true;
+    rbuf = 0;
+}
+
+// R_PEND -> R: the fused kernel in residual-only mode over the Q buffer that
+// held the last residual's input (its ghost planes were fresh for that
+// substep and nothing has written it since).  Bitwise the R that substep
+// computed: R depends on Q only.
+void Solver::materialize_r() {
+    if (r_state != R_PEND) return;
+    ensure_r();
+    const PrimConsts pc = prim_consts();
+    const ResConsts rc = res_consts();
+    const StageConsts sc = stage_consts();
+    RkConsts kc{};
+    kc.skip_a = 1;
+    const bool staged = strategy == MPFD_DEFAULT && viscous;
+    sync();
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        const void* qin = qbuf_ptr(s, r_src);
+        launch->fused(s, qin, nullptr, qtcur(s), nullptr, rcur(s), pc, rc, sc, staged, kc, 2, 0, 0, 0, s.geo.nzl);
+        CK(cudaGetLastError());
+    }
+    sync();
+    reset_div();
+    r_state = R_MAT;
+}
+
+void Solver::set_exact(bool on) {
+    if (on == exact) return;
+    sync();
+    materialize_r();
+    const size_t bt = byte_width(plan.tk), br = byte_width(plan.rk);
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        const size_t tb = (size_t)s.geo.nzl * 5 * s.geo.plane * bt;
+        const size_t rb = (size_t)s.geo.nzl * 5 * s.geo.plane * br;
+        if (on) {
+            // both Qt buffers hold the current Qt; R moves to buffer 0
+            if (fused_ok && !s.qt2) {
+                CK(cudaMalloc(&s.qt2, tb));
+                s.bytes += tb;
+            }
+            if (s.qt2) CK(cudaMemcpyAsync(s.qt2, s.qt, tb, cudaMemcpyDeviceToDevice, s.stream));
+            if (r_alloc && !s.r2) {
+                CK(cudaMalloc(&s.r2, rb));
+                CK(cudaMemsetAsync(s.r2, 0, rb, s.stream));
+                s.bytes += rb;
+            }
+        } else {
+            if (use_fused() && qbuf && s.qt2)
+                CK(cudaMemcpyAsync(s.qt, s.qt2, tb, cudaMemcpyDeviceToDevice, s.stream));
+            if (r_alloc && rbuf && s.r2) CK(cudaMemcpyAsync(s.r, s.r2, rb, cudaMemcpyDeviceToDevice, s.stream));
+            for (void** p : {&s.qt2, &s.r2}) {
+                if (!*p) continue;
+                CK(cudaStreamSynchronize(s.stream));
+                CK(cudaFree(*p));
+                *p = nullptr;
+                s.bytes -= p == &s.qt2 ? tb : rb;
+            }
+        }
+    }
+    rbuf = 0;
+    exact = on;
+    sync();
+}
+
+// exact mode: no slab starts substep s+1 before every slab has finished s
+// (and seen its divergence record): LOCAL slabs wait on each other's
+// completion events (one shared record per device); NCCL ranks min-reduce
+// the record's key on the stream, so a later substep's launches are no-ops
+// on every rank once any rank has diverged
+void Solver::substep_barrier() {
+    if (!exact) return;
+    if (mode == MPFD_DECOMP_NCCL) {
+        Slab& s = slabs[0];
+        CK(cudaSetDevice(s.device));
+        Nccl& nc = Nccl::get();
+        nc.check(nc.allReduce(&s.div->key, &s.div->key, 1, 5 /*uint64*/, 3 /*min*/, comm, s.stream),
+                 "ncclAllReduce");
+        return;
+    }
+    if (slabs.size() < 2) return;
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        CK(cudaEventRecord(s.ev_d, s.stream));
+    }
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        for (auto& o : slabs)
+            if (&o != &s) CK(cudaStreamWaitEvent(s.stream, o.ev_d, 0));
+    }
 }
 
 static void alloc_staged(Solver& S) {
@@ -401,10 +548,11 @@ static void alloc_staged(Solver& S) {
 
 void Solver::reset_div() {
     DevDiv d;
-    std::memset(&d, 0, sizeof d);
+    d.key = ULLONG_MAX;
     for (auto& row : d.idx)
         for (auto& v : row) v = ULLONG_MAX;
     for (auto& s : slabs) {
+        if (!s.owns_div) continue;
         CK(cudaSetDevice(s.device));
         CK(cudaMemcpyAsync(s.div, &d, sizeof d, cudaMemcpyHostToDevice, s.stream));
         CK(cudaStreamSynchronize(s.stream));
@@ -501,20 +649,22 @@ static void with_kind(int k, F&& f) {
 }
 
 // cls 0 Q, 1 Qt, 2 R.  src indexes this slab's local point (i,j,k) at
-// k*ld_plane + j*ld_row + i (binary64 carriers); rounded on the device
-void Solver::upload_slab(Slab& s, int cls, int comp, const double* src, size_t ld_row, size_t ld_plane) {
+// k*ld_plane + j*ld_row + i (binary64 carriers), for local planes
+// [zb, zb + nz); rounded on the device
+void Solver::upload_planes(Slab& s, int cls, int comp, const double* src, size_t ld_row, size_t ld_plane, int zb,
+                           int nz) {
     if (cls < 0 || cls > 2 || comp < 0 || comp > 4) throw ConfigError("bad class/component");
     const int kind = cls == 0 ? plan.qk : (cls == 1 ? plan.tk : plan.rk);
     CK(cudaSetDevice(s.device));
     const long long pl = s.geo.plane;
     const int planes_per = (int)std::max<size_t>(1, s.staging_elems / pl);
-    for (int z = 0; z < s.geo.nzl; z += planes_per) {
-        const int nzc = std::min(planes_per, s.geo.nzl - z);
+    for (int z = zb; z < zb + nz; z += planes_per) {
+        const int nzc = std::min(planes_per, zb + nz - z);
         for (int zz = 0; zz < nzc; ++zz)
             CK(cudaMemcpy2DAsync(s.staging + (size_t)zz * pl, (size_t)n * sizeof(double),
                                  src + (size_t)(z + zz) * ld_plane, ld_row * sizeof(double),
                                  (size_t)n * sizeof(double), n, cudaMemcpyHostToDevice, s.stream));
-        void* base = cls == 0 ? qcur(s) : (cls == 1 ? qtcur(s) : s.r);
+        void* base = cls == 0 ? qcur(s) : (cls == 1 ? qtcur(s) : rcur(s));
         const long long count = (long long)nzc * pl;
         const long long zoff = cls == 0 ? z + kHalo : z;
         with_kind(kind, [&](auto tag) {
@@ -529,20 +679,40 @@ void Solver::upload_slab(Slab& s, int cls, int comp, const double* src, size_t l
     if (cls == 0) halo_fresh = false;
 }
 
+void Solver::upload_slab(Slab& s, int cls, int comp, const double* src, size_t ld_row, size_t ld_plane) {
+    upload_planes(s, cls, comp, src, ld_row, ld_plane, 0, s.geo.nzl);
+}
+
 void Solver::set_interior(int cls, int comp, const double* src, size_t ld_row, size_t ld_plane, int off) {
+    if (cls == 2) {
+        // a partial write keeps the rest of R as it is
+        materialize_r();
+        ensure_r();
+        r_state = R_MAT;
+    }
     for (auto& s : slabs) upload_slab(s, cls, comp, src + off + (size_t)s.geo.z0 * ld_plane, ld_row, ld_plane);
 }
 
 void Solver::get_interior(int cls, int comp, double* dst, size_t ld_row, size_t ld_plane, int off) {
     if (cls < 0 || cls > 2 || comp < 0 || comp > 4) throw ConfigError("bad class/component");
     const int kind = cls == 0 ? plan.qk : (cls == 1 ? plan.tk : plan.rk);
+    if (cls == 2) materialize_r();
+    if (cls == 2 && !r_alloc) {
+        // zero_temporaries (tgv.cpp:22-25): R has never been written
+        for (auto& s : slabs)
+            for (int z = 0; z < s.geo.nzl; ++z)
+                for (int y = 0; y < n; ++y)
+                    std::memset(dst + off + (size_t)(s.geo.z0 + z) * ld_plane + (size_t)y * ld_row, 0,
+                                (size_t)n * sizeof(double));
+        return;
+    }
     for (auto& s : slabs) {
         CK(cudaSetDevice(s.device));
         const long long pl = s.geo.plane;
         const int planes_per = (int)std::max<size_t>(1, s.staging_elems / pl);
         for (int z = 0; z < s.geo.nzl; z += planes_per) {
             const int nzc = std::min(planes_per, s.geo.nzl - z);
-            const void* base = cls == 0 ? qcur(s) : (cls == 1 ? qtcur(s) : s.r);
+            const void* base = cls == 0 ? qcur(s) : (cls == 1 ? qtcur(s) : rcur(s));
             const long long count = (long long)nzc * pl;
             with_kind(kind, [&](auto tag) {
                 using S = decltype(tag);
@@ -574,49 +744,55 @@ void Solver::init(int case_kind) {
     const double h_ = h;
     const double p_ref = 1.0 / gm2;
     qbuf = 0;
+    rbuf = 0;
     for (auto& s : slabs) {
-        // this slab's planes only, [nzl][n][n]
+        // this slab's planes, in chunks of at most ~1.3 GB of binary64
+        // carriers (so a 1024^3 slab needs no 43 GB host copy)
         const size_t z0 = (size_t)s.geo.z0, nzl_ = (size_t)s.geo.nzl;
+        const size_t chunk = std::max<size_t>(1, std::min<size_t>(nzl_, ((size_t)1 << 25) / pl));
         std::vector<double> f[5];
-        for (auto& v : f) v.assign(nzl_ * pl, 0.0);
-        auto fill_planes = [&](size_t k0, size_t k1) {
-            for (size_t k = k0; k < k1; ++k) {
-                // z periods > 1 (weak scaling) repeat the 2 pi-periodic
-                // field: plane k takes the values of plane k mod n exactly
-                const double z = (double)((z0 + k) % (size_t)n) * h_;
-                for (int j = 0; j < n; ++j) {
-                    const double y = j * h_;
-                    for (int i = 0; i < n; ++i) {
-                        const size_t o = (k * n + j) * n + i;
-                        if (case_kind == 1) {
-                            const double p0 = 1.0 / gm2;
-                            f[0][o] = gm2 * p0;
-                            f[1][o] = f[2][o] = f[3][o] = 0.0;
-                            f[4][o] = p0 / (g - 1.0);
-                            continue;
+        for (auto& v : f) v.assign(chunk * pl, 0.0);
+        for (size_t c0 = 0; c0 < nzl_; c0 += chunk) {
+            const size_t nc = std::min(chunk, nzl_ - c0);
+            auto fill_planes = [&](size_t k0, size_t k1) {
+                for (size_t k = k0; k < k1; ++k) {
+                    // z periods > 1 (weak scaling) repeat the 2 pi-periodic
+                    // field: plane k takes the values of plane k mod n exactly
+                    const double z = (double)((z0 + c0 + k) % (size_t)n) * h_;
+                    for (int j = 0; j < n; ++j) {
+                        const double y = j * h_;
+                        for (int i = 0; i < n; ++i) {
+                            const size_t o = (k * n + j) * n + i;
+                            if (case_kind == 1) {
+                                const double p0 = 1.0 / gm2;
+                                f[0][o] = gm2 * p0;
+                                f[1][o] = f[2][o] = f[3][o] = 0.0;
+                                f[4][o] = p0 / (g - 1.0);
+                                continue;
+                            }
+                            const double x = i * h_;
+                            const double u = std::sin(x) * std::cos(y) * std::cos(z);
+                            const double v = -std::cos(x) * std::sin(y) * std::cos(z);
+                            const double p = p_ref + (1.0 / 16.0) * (std::cos(2 * x) + std::cos(2 * y)) *
+                                                         (2.0 + std::cos(2 * z));
+                            const double rho = gm2 * p;
+                            const double rhoE = p / (g - 1.0) + 0.5 * rho * (u * u + v * v);
+                            f[0][o] = rho;
+                            f[1][o] = rho * u;
+                            f[2][o] = rho * v;
+                            f[3][o] = 0.0;
+                            f[4][o] = rhoE;
                         }
-                        const double x = i * h_;
-                        const double u = std::sin(x) * std::cos(y) * std::cos(z);
-                        const double v = -std::cos(x) * std::sin(y) * std::cos(z);
-                        const double p = p_ref + (1.0 / 16.0) * (std::cos(2 * x) + std::cos(2 * y)) *
-                                                     (2.0 + std::cos(2 * z));
-                        const double rho = gm2 * p;
-                        const double rhoE = p / (g - 1.0) + 0.5 * rho * (u * u + v * v);
-                        f[0][o] = rho;
-                        f[1][o] = rho * u;
-                        f[2][o] = rho * v;
-                        f[3][o] = 0.0;
-                        f[4][o] = rhoE;
                     }
                 }
-            }
-        };
-        const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-        std::vector<std::thread> th;
-        for (unsigned t = 0; t < nt; ++t)
-            th.emplace_back(fill_planes, nzl_ * t / nt, nzl_ * (t + 1) / nt);
-        for (auto& t : th) t.join();
-        for (int comp = 0; comp < 5; ++comp) upload_slab(s, 0, comp, f[comp].data(), n, pl);
+            };
+            const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+            std::vector<std::thread> th;
+            for (unsigned t = 0; t < nt; ++t) th.emplace_back(fill_planes, nc * t / nt, nc * (t + 1) / nt);
+            for (auto& t : th) t.join();
+            for (int comp = 0; comp < 5; ++comp)
+                upload_planes(s, 0, comp, f[comp].data() - c0 * pl, n, pl, (int)c0, (int)nc);
+        }
     }
     halo_fresh = false;
     // Qt and R zeroed (zero_temporaries, tgv.cpp:22-25)
@@ -624,9 +800,11 @@ void Solver::init(int case_kind) {
         CK(cudaSetDevice(s.device));
         const size_t iel = (size_t)s.geo.nzl * 5 * s.geo.plane;
         CK(cudaMemsetAsync(s.qt, 0, iel * byte_width(plan.tk), s.stream));
-        CK(cudaMemsetAsync(s.r, 0, iel * byte_width(plan.rk), s.stream));
         if (s.qt2) CK(cudaMemsetAsync(s.qt2, 0, iel * byte_width(plan.tk), s.stream));
+        if (s.r) CK(cudaMemsetAsync(s.r, 0, iel * byte_width(plan.rk), s.stream));
+        if (s.r2) CK(cudaMemsetAsync(s.r2, 0, iel * byte_width(plan.rk), s.stream));
     }
+    r_state = R_ZERO;
     reset_div();
     halo_refresh();
     sync();
@@ -808,6 +986,7 @@ void Solver::flush_profile() {
 void Solver::residual_enqueue(int iter, int sub) {
     if (!halo_fresh) halo_refresh();
     alloc_staged(*this);
+    ensure_r();
     const PrimConsts pc = prim_consts();
     const ResConsts rc = res_consts();
     const StageConsts sc = stage_consts();
@@ -816,179 +995,178 @@ void Solver::residual_enqueue(int iter, int sub) {
         CK(cudaSetDevice(s.device));
         Slab view = s;
         view.q = qcur(s);
+        view.r = rcur(s);
         timed(3, s, [&] { launch->prim(view, pc, iter, sub); });
         if (viscous) timed(3, s, [&] { launch->level2(view, rc, sc, staged); });
         timed(0, s, [&] { launch->resid(view, rc, iter, sub); });
         CK(cudaGetLastError());
     }
+    r_state = R_MAT;
 }
 
 void Solver::rk_enqueue(int sub, const double a[3], const double b[3], double dt, int iter) {
     const RkConsts kc = rk_consts(sub, a, b, dt);
+    materialize_r();
+    ensure_r();
     for (auto& s : slabs) {
         CK(cudaSetDevice(s.device));
         Slab view = s;
         view.q = qcur(s);
         view.qt = qtcur(s);
+        view.r = rcur(s);
         timed(1, s, [&] { launch->rk(view, kc, iter, sub); });
         CK(cudaGetLastError());
     }
     halo_fresh = false;
 }
 
-// one substep of advance's inner loop: evaluate -> rk_substep -> halo fill
-void Solver::substep_enqueue(int sub, const double a[3], const double b[3], double dt, int iter,
-                             bool write_r) {
-    if (overlap_ok()) {
-        // interior planes [H, nzl-H) need no ghost plane: they run while the
-        // exchange is in flight; the 2H boundary planes follow it
-        const bool need_x = !halo_fresh;
-        if (need_x) exchange_async();
-        const PrimConsts pc = prim_consts();
-        const ResConsts rc = res_consts();
-        const StageConsts sc = stage_consts();
-        const RkConsts kc = rk_consts(sub, a, b, dt);
-        const bool staged = strategy == MPFD_DEFAULT && viscous;
-        for (auto& s : slabs) {
-            CK(cudaSetDevice(s.device));
-            const void* qin = qbuf ? s.q2 : s.q;
-            void* qout = qbuf ? s.q : s.q2;
-            const void* qtin = qbuf ? s.qt2 : s.qt;
-            void* qtout = qbuf ? s.qt : s.qt2;
-            const int nz = s.geo.nzl;
+// one substep of advance's inner loop: evaluate -> rk_substep -> halo fill.
+// Fused path: Q ping-pongs between two buffers (neighbouring CTAs read the
+// old Q at reach 4); Qt is updated in place (read only at its own point);
+// R is not written -- it stays pending on the input buffer (materialize_r)
+// -- except in exact mode, where Qt and R ping-pong too.
+void Solver::substep_enqueue(int sub, const double a[3], const double b[3], double dt, int iter) {
+    if (!use_fused()) {
+        if (!halo_fresh) halo_refresh();
+        residual_enqueue(iter, sub);
+        rk_enqueue(sub, a, b, dt, iter);
+        halo_refresh();
+        substep_barrier();
+        return;
+    }
+    const bool ov = overlap_ok();
+    const bool need_x = ov && !halo_fresh;
+    if (need_x) exchange_async();
+    else if (!halo_fresh) halo_refresh();
+    const PrimConsts pc = prim_consts();
+    const ResConsts rc = res_consts();
+    const StageConsts sc = stage_consts();
+    const RkConsts kc = rk_consts(sub, a, b, dt);
+    const bool staged = strategy == MPFD_DEFAULT && viscous;
+    if (exact) ensure_r();
+    const int write_r = exact ? 1 : 0;
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        const void* qin = qbuf_ptr(s, qbuf);
+        void* qout = qbuf_ptr(s, qbuf ^ 1);
+        const void* qtin = exact && qbuf ? s.qt2 : s.qt;
+        void* qtout = exact ? (qbuf ? s.qt : s.qt2) : s.qt;
+        void* rout = exact ? (rbuf ? s.r : s.r2) : nullptr;
+        const int nz = s.geo.nzl;
+        if (ov) {
+            // interior planes [H, nzl-H) need no ghost plane: they run while
+            // the exchange is in flight; the 2H boundary planes follow it
             timed(0, s, [&] {
-                launch->fused(s, qin, qout, qtin, qtout, pc, rc, sc, staged, kc, write_r, iter, sub, kHalo,
+                launch->fused(s, qin, qout, qtin, qtout, rout, pc, rc, sc, staged, kc, write_r, iter, sub, kHalo,
                               nz - kHalo);
             });
             if (need_x) CK(cudaStreamWaitEvent(s.stream, s.ev_x, 0));
             timed(0, s, [&] {
-                launch->fused(s, qin, qout, qtin, qtout, pc, rc, sc, staged, kc, write_r, iter, sub, 0, kHalo);
-                launch->fused(s, qin, qout, qtin, qtout, pc, rc, sc, staged, kc, write_r, iter, sub, nz - kHalo,
-                              nz);
+                launch->fused(s, qin, qout, qtin, qtout, rout, pc, rc, sc, staged, kc, write_r, iter, sub, 0, kHalo);
+                launch->fused(s, qin, qout, qtin, qtout, rout, pc, rc, sc, staged, kc, write_r, iter, sub,
+                              nz - kHalo, nz);
             }, 2);
-            CK(cudaGetLastError());
-        }
-        qbuf ^= 1;
-        halo_fresh = false;
-        return;
-    }
-    if (!halo_fresh) halo_refresh();
-    if (use_fused()) {
-        const PrimConsts pc = prim_consts();
-        const ResConsts rc = res_consts();
-        const StageConsts sc = stage_consts();
-        const RkConsts kc = rk_consts(sub, a, b, dt);
-        const bool staged = strategy == MPFD_DEFAULT && viscous;
-        for (auto& s : slabs) {
-            CK(cudaSetDevice(s.device));
-            const void* qin = qbuf ? s.q2 : s.q;
-            void* qout = qbuf ? s.q : s.q2;
-            const void* qtin = qbuf ? s.qt2 : s.qt;
-            void* qtout = qbuf ? s.qt : s.qt2;
+        } else {
             timed(0, s, [&] {
-                launch->fused(s, qin, qout, qtin, qtout, pc, rc, sc, staged, kc, write_r, iter, sub, 0,
-                              s.geo.nzl);
+                launch->fused(s, qin, qout, qtin, qtout, rout, pc, rc, sc, staged, kc, write_r, iter, sub, 0, nz);
             });
-            CK(cudaGetLastError());
         }
-        qbuf ^= 1;
-        halo_fresh = false;
-    } else {
-        residual_enqueue(iter, sub);
-        rk_enqueue(sub, a, b, dt, iter);
+        CK(cudaGetLastError());
     }
-    halo_refresh();
+    if (exact) {
+        rbuf ^= 1;
+        r_state = R_MAT;
+    } else {
+        r_state = R_PEND;
+        r_src = qbuf;
+    }
+    qbuf ^= 1;
+    halo_fresh = false;
+    // without overlap the ghost planes are refreshed right away (the
+    // reference's fill_state_halos); with it, by the next substep's exchange
+    if (!ov) halo_refresh();
+    substep_barrier();
 }
 
-// true if any slab recorded a divergence (block: synchronous read)
+// true if any slab (any rank) recorded a divergence (block: synchronous read;
+// non-blocking: only when every stream has drained)
 bool Solver::poll_div(bool block) {
-    int any = 0;
     for (size_t i = 0; i < slabs.size(); ++i) {
         Slab& s = slabs[i];
         CK(cudaSetDevice(s.device));
-        CK(cudaMemcpyAsync(pinned_flag + i, &s.div->flag, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+        CK(cudaMemcpyAsync(pinned + i, &s.div->key, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s.stream));
     }
     if (!block) {
-        // cheap check: only look if all streams already drained
         for (auto& s : slabs)
             if (cudaStreamQuery(s.stream) != cudaSuccess) return false;
     } else {
         sync();
     }
-    for (size_t i = 0; i < slabs.size(); ++i) any |= pinned_flag[i];
+    unsigned long long key = ULLONG_MAX;
+    for (size_t i = 0; i < slabs.size(); ++i) key = std::min(key, pinned[i]);
     if (mode == MPFD_DECOMP_NCCL && block) {
-        int* d = nullptr;
+        // every rank polls at the same iterations (the schedule is
+        // deterministic), so this collective pairs up
         Slab& s = slabs[0];
-        CK(cudaMalloc(&d, sizeof(int)));
-        CK(cudaMemcpyAsync(d, &any, sizeof(int), cudaMemcpyHostToDevice, s.stream));
+        pinned[0] = key;
+        CK(cudaMemcpyAsync(s.red, pinned, sizeof(unsigned long long), cudaMemcpyHostToDevice, s.stream));
         Nccl& nc = Nccl::get();
-        nc.check(nc.allReduce(d, d, 1, 2 /*int32*/, 2 /*max*/, comm, s.stream), "ncclAllReduce");
-        CK(cudaMemcpyAsync(&any, d, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+        nc.check(nc.allReduce(s.red, s.red, 1, 5 /*uint64*/, 3 /*min*/, comm, s.stream), "ncclAllReduce");
+        CK(cudaMemcpyAsync(pinned, s.red, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s.stream));
         CK(cudaStreamSynchronize(s.stream));
-        cudaFree(d);
+        key = pinned[0];
     }
-    return any != 0;
+    return key != ULLONG_MAX;
 }
 
-// reduce the per-slab first-in-scan-order records into one DivergenceEvent
+// Merge the per-slab (per-rank) records into one DivergenceEvent: the
+// earliest substep any slab recorded, and inside it the reference's check
+// order -- density (primitives) -> nonfinite residual -> nonfinite state,
+// components in order, first point in scan order.  Records of later
+// substeps (a slab that ran ahead before it saw the event) carry a larger
+// key and drop out of the minimum.
 bool Solver::resolve_div(mpfd_divergence* ev, double dt) {
     sync();
-    DevDiv tot;
-    std::memset(&tot, 0, sizeof tot);
-    for (auto& row : tot.idx)
-        for (auto& v : row) v = ULLONG_MAX;
-    long long best = LLONG_MAX;
+    unsigned long long tot[15];
+    for (auto& v : tot) v = ULLONG_MAX;
     for (auto& s : slabs) {
-        DevDiv d;
+        if (!s.owns_div) continue;
         CK(cudaSetDevice(s.device));
-        CK(cudaMemcpy(&d, s.div, sizeof d, cudaMemcpyDeviceToHost));
-        if (!d.flag) continue;
-        tot.flag = 1;
-        const long long key = (long long)d.iter * 3 + d.sub;
-        if (key < best) {
-            best = key;
-            tot.iter = d.iter;
-            tot.sub = d.sub;
-        }
+        DevDiv* d = reinterpret_cast<DevDiv*>(pinned + 16);
+        CK(cudaMemcpyAsync(d, s.div, sizeof(DevDiv), cudaMemcpyDeviceToHost, s.stream));
+        CK(cudaStreamSynchronize(s.stream));
         for (int a = 0; a < 3; ++a)
-            for (int b = 0; b < 5; ++b) tot.idx[a][b] = std::min(tot.idx[a][b], d.idx[a][b]);
+            for (int b = 0; b < 5; ++b) tot[a * 5 + b] = std::min(tot[a * 5 + b], d->idx[a][b]);
     }
     if (mode == MPFD_DECOMP_NCCL) {
-        // global min over ranks of (iteration, substep) and the index table
-        unsigned long long buf[16];
-        buf[0] = tot.flag ? (unsigned long long)tot.iter * 3 + tot.sub : ULLONG_MAX;
-        for (int a = 0; a < 3; ++a)
-            for (int b = 0; b < 5; ++b) buf[1 + a * 5 + b] = tot.idx[a][b];
-        unsigned long long* d = nullptr;
         Slab& s = slabs[0];
-        CK(cudaMalloc(&d, sizeof buf));
-        CK(cudaMemcpy(d, buf, sizeof buf, cudaMemcpyHostToDevice));
+        std::memcpy(pinned, tot, sizeof tot);
+        CK(cudaMemcpyAsync(s.red, pinned, sizeof tot, cudaMemcpyHostToDevice, s.stream));
         Nccl& nc = Nccl::get();
-        nc.check(nc.allReduce(d, d, 16, 5 /*uint64*/, 3 /*min*/, comm, s.stream), "ncclAllReduce");
-        CK(cudaMemcpy(buf, d, sizeof buf, cudaMemcpyDeviceToHost));
-        cudaFree(d);
-        if (buf[0] == ULLONG_MAX) return false;
-        tot.flag = 1;
-        tot.iter = (int)(buf[0] / 3);
-        tot.sub = (int)(buf[0] % 3);
-        for (int a = 0; a < 3; ++a)
-            for (int b = 0; b < 5; ++b) tot.idx[a][b] = buf[1 + a * 5 + b];
+        nc.check(nc.allReduce(s.red, s.red, 15, 5 /*uint64*/, 3 /*min*/, comm, s.stream), "ncclAllReduce");
+        CK(cudaMemcpyAsync(pinned, s.red, sizeof tot, cudaMemcpyDeviceToHost, s.stream));
+        CK(cudaStreamSynchronize(s.stream));
+        std::memcpy(tot, pinned, sizeof tot);
     }
-    if (!tot.flag) return false;
-    // priority of the reference's checks: density (primitives) -> nonfinite
-    // residual -> nonfinite state; components in order, scan order inside
+    unsigned long long best = ULLONG_MAX;
+    for (auto v : tot)
+        if (v != ULLONG_MAX) best = std::min(best, v >> kDivKeyShift);
+    if (best == ULLONG_MAX) return false;
+    const unsigned long long mask = (1ull << kDivKeyShift) - 1;
     for (int code = 0; code < 3; ++code)
         for (int comp = 0; comp < 5; ++comp) {
-            const unsigned long long gi = tot.idx[code][comp];
-            if (gi == ULLONG_MAX) continue;
+            const unsigned long long v = tot[code * 5 + comp];
+            if (v == ULLONG_MAX || (v >> kDivKeyShift) != best) continue;
+            const unsigned long long gi = v & mask;
             if (ev) {
+                const long iter = (long)(best / 3);
                 ev->code = code + 1;
                 ev->i = (int)(gi % (unsigned long long)n);
                 ev->j = (int)((gi / n) % (unsigned long long)n);
                 ev->k = (int)(gi / ((unsigned long long)n * n));
-                ev->iteration = tot.iter;
-                ev->substep = tot.sub;
-                ev->time = code == 2 ? (tot.iter + 1) * dt : tot.iter * dt;
+                ev->iteration = iter;
+                ev->substep = (int)(best % 3);
+                ev->time = code == 2 ? (iter + 1) * dt : iter * dt;
             }
             return true;
         }
@@ -1003,63 +1181,64 @@ void Solver::diagnostics(int weighting, double t, int threads, mpfd_diag* out) {
     const size_t nch_total = N / 4096;
     bool aligned = ((size_t)nzl() * n * n) % 4096 == 0 && N >= 4096;
     if (aligned && threads <= 1 && (nch_total & (nch_total - 1)) != 0) aligned = false;
+    const double r = 1.0 / (12.0 * h);
     double sums[2];
     for (int which = 0; which < 2; ++which) {
-        std::vector<double> parts;  // global-order chunk sums, or the full integrand
+        // global-order chunk sums (aligned), else the whole integrand
+        std::vector<double> parts;
         for (auto& s : slabs) {
             CK(cudaSetDevice(s.device));
             Slab view = s;
             view.q = qcur(s);
-            launch->diag_integrand(view, which, weighting, 1.0 / (12.0 * h));
-            CK(cudaGetLastError());
             const size_t nint = (size_t)s.geo.nzl * s.geo.plane;
+            const double* src;
+            size_t cnt;
             if (aligned) {
-                const long long nch = (long long)(nint / 4096);
-                k_chunk_sums<<<(unsigned)((nch * 32 + 255) / 256), 256, 0, s.stream>>>(s.diag, nch, s.partials);
-                CK(cudaGetLastError());
-                const size_t o = parts.size();
-                parts.resize(o + nch);
-                CK(cudaMemcpyAsync(parts.data() + o, s.partials, nch * sizeof(double), cudaMemcpyDeviceToHost,
-                                   s.stream));
+                cnt = nint / 4096;
+                launch->diag_chunks(view, which, weighting, r, (long long)cnt, s.partials);
+                src = s.partials;
             } else {
-                const size_t o = parts.size();
-                parts.resize(o + nint);
-                CK(cudaMemcpyAsync(parts.data() + o, s.diag, nint * sizeof(double), cudaMemcpyDeviceToHost,
-                                   s.stream));
+                if (!s.diag) {
+                    CK(cudaMalloc(&s.diag, nint * sizeof(double)));
+                    s.bytes += nint * sizeof(double);
+                    view.diag = s.diag;
+                }
+                cnt = nint;
+                launch->diag_integrand(view, which, weighting, r);
+                src = s.diag;
             }
+            CK(cudaGetLastError());
+            if (mode == MPFD_DECOMP_NCCL) {
+                // every rank's parts in rank (= global z) order, device to device
+                if (s.gather_elems < cnt * pz) {
+                    cudaFree(s.gather);
+                    CK(cudaMalloc(&s.gather, cnt * pz * sizeof(double)));
+                    s.gather_elems = cnt * pz;
+                }
+                Nccl& nc = Nccl::get();
+                nc.check(nc.allGather(src, s.gather, cnt, 8 /*float64*/, comm, s.stream), "ncclAllGather");
+                src = s.gather;
+                cnt *= pz;
+            }
+            const size_t o = parts.size();
+            parts.resize(o + cnt);
+            CK(cudaMemcpyAsync(parts.data() + o, src, cnt * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
             CK(cudaStreamSynchronize(s.stream));
-        }
-        if (mode == MPFD_DECOMP_NCCL) {
-            // gather every rank's parts in rank (= global z) order
-            Slab& s = slabs[0];
-            const size_t cnt = parts.size();
-            double* d = nullptr;
-            CK(cudaMalloc(&d, cnt * pz * sizeof(double)));
-            CK(cudaMemcpy(d + cnt * rank, parts.data(), cnt * sizeof(double), cudaMemcpyHostToDevice));
-            Nccl& nc = Nccl::get();
-            nc.check(nc.allGather(d + cnt * rank, d, cnt, 8 /*float64*/, comm, s.stream), "ncclAllGather");
-            parts.resize(cnt * pz);
-            CK(cudaMemcpyAsync(parts.data(), d, cnt * pz * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
-            CK(cudaStreamSynchronize(s.stream));
-            cudaFree(d);
         }
         double sum;
         if (aligned) {
             const size_t nch = parts.size();
-            const bool pow2 = (nch & (nch - 1)) == 0;
             if (N <= 4096) sum = parts[0];
             else if (threads > 1) sum = pairwise_sum(parts.data(), nch);
             else sum = tree_of_chunks(parts.data(), nch);  // nch is a power of two here
-            (void)pow2;
+        } else if (threads > 1 && N > 4096) {
+            const size_t nch = (N + 4095) / 4096;
+            std::vector<double> c(nch);
+            for (size_t i = 0; i < nch; ++i)
+                c[i] = pairwise_sum(parts.data() + i * 4096, std::min<size_t>(4096, N - i * 4096));
+            sum = pairwise_sum(c.data(), nch);
         } else {
-            if (threads > 1 && N > 4096) {
-                const size_t nch = (N + 4095) / 4096;
-                std::vector<double> c(nch);
-                for (size_t i = 0; i < nch; ++i) c[i] = pairwise_sum(parts.data() + i * 4096, std::min<size_t>(4096, N - i * 4096));
-                sum = pairwise_sum(c.data(), nch);
-            } else {
-                sum = pairwise_sum(parts.data(), N);
-            }
+            sum = pairwise_sum(parts.data(), N);
         }
         sums[which] = sum;
     }
@@ -1280,6 +1459,8 @@ int mpfd_b200_diagnostics(mpfd_solver* h, int weighting, double t, int threads, 
 static void check_step(const mpfd_step* st) {
     if (!st) throw ConfigError("null step");
     if (!(st->dt > 0)) throw ConfigError("dt must be positive");
+    // divergence records carry iteration * 3 + substep in 25 bits
+    if (st->n_iterations > (1L << 25) / 3 - 1) throw ConfigError("n_iterations exceeds 11184809 per advance call");
 }
 
 // write_snapshot (io.cpp:69-85): int32 {n, n, n, 5}, then the five
@@ -1335,10 +1516,11 @@ int mpfd_b200_advance(mpfd_solver* h, const mpfd_step* st, mpfd_diag* series, lo
             d.ke_normalized = k0 != 0.0 ? d.kinetic_energy / k0 : 0.0;
             series[count++] = d;
         };
+        const auto t_start = std::chrono::steady_clock::now();
         S.reset_div();
         S.halo_refresh();
         sample(0.0, false);
-        const int qbuf_start = S.qbuf;
+        const int qbuf_start = S.qbuf, rbuf_start = S.rbuf;
         long done = 0;
         int status = MPFD_OK;
         mpfd_divergence e{};
@@ -1348,7 +1530,7 @@ int mpfd_b200_advance(mpfd_solver* h, const mpfd_step* st, mpfd_diag* series, lo
             const bool last = it + 1 == st->n_iterations;
             const double t_next = (double)(it + 1) * st->dt;
             for (int sub = 0; sub < 3; ++sub)
-                S.substep_enqueue(sub, st->a, st->b, st->dt, (int)it, last && sub == 2);
+                S.substep_enqueue(sub, st->a, st->b, st->dt, (int)it);
             const bool due = st->diagnostics_interval > 0 && (it + 1) % st->diagnostics_interval == 0;
             // snapshot rule of advance (integrate.cpp:154-158)
             const bool snap = next_snap < S.snap_times.size() && t_next >= S.snap_times[next_snap] - 0.5 * st->dt;
@@ -1357,20 +1539,26 @@ int mpfd_b200_advance(mpfd_solver* h, const mpfd_step* st, mpfd_diag* series, lo
                 S.resolve_div(&e, st->dt);
                 status = MPFD_DIVERGED;
                 done = e.iteration;
-                // the fused path double-buffers Q and Qt: the state the reference
-                // holds at the event is the input of the failing substep (density /
+                // The fused path double-buffers Q: the state the reference holds
+                // at the event is the input of the failing substep (density /
                 // residual signal) or its output (nonfinite state); every launched
-                // substep flipped the buffer index, no-op launches included
+                // substep flipped the buffer index, no-op launches included.  R:
+                // the failing substep's residual (codes 2, 3) or the previous
+                // one's (code 1, the reference returns before it computes R).
+                // Exact mode ping-pongs Qt and R the same way, so all three are
+                // the reference's; by default Qt is updated in place (exact for
+                // code 3 only) and R is recomputed from the failing substep's
+                // input buffer (exact for codes 2 and 3).
                 if (S.use_fused()) {
                     const long failed = e.iteration * 3 + e.substep;
                     const long keep = e.code == 3 ? failed + 1 : failed;
                     S.qbuf = qbuf_start ^ (int)(keep & 1);
-                    if (e.code == 2) {
-                        // R as the reference leaves it: the nonfinite residual
-                        S.reset_div();
-                        S.halo_fresh = false;
-                        S.residual_enqueue((int)e.iteration, e.substep);
-                        S.sync();
+                    if (S.exact) {
+                        S.rbuf = rbuf_start ^ (int)((e.code == 1 ? failed : failed + 1) & 1);
+                        S.r_state = Solver::R_MAT;
+                    } else {
+                        S.r_state = Solver::R_PEND;
+                        S.r_src = qbuf_start ^ (int)(failed & 1);
                     }
                 }
                 S.halo_fresh = false;
@@ -1392,6 +1580,10 @@ int mpfd_b200_advance(mpfd_solver* h, const mpfd_step* st, mpfd_diag* series, lo
             }
         }
         S.sync();
+        // wall time around the whole call (integrate.cpp:102, 162-165)
+        S.last_wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+        S.last_iters = done;
+        S.last_spi = done > 0 ? S.last_wall / (double)done : 0.0;
         if (len) *len = count;
         if (iters) *iters = done;
         if (ev) *ev = e;
@@ -1413,7 +1605,7 @@ int mpfd_b200_run_steps(mpfd_solver* h, const mpfd_step* st, long iters) {
         check_step(st);
         Solver& S = h->s;
         for (long it = 0; it < iters; ++it)
-            for (int sub = 0; sub < 3; ++sub) S.substep_enqueue(sub, st->a, st->b, st->dt, (int)it, false);
+            for (int sub = 0; sub < 3; ++sub) S.substep_enqueue(sub, st->a, st->b, st->dt, (int)it);
         return MPFD_OK;
     });
 }
@@ -1439,6 +1631,52 @@ int mpfd_b200_profile_read(mpfd_solver* h, double ms[4], long launches[4]) {
             ms[c] = S.prof_ms[c];
             launches[c] = S.prof_launch[c];
         }
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_set_exact_divergence(mpfd_solver* h, int enable) {
+    return guard([&] {
+        h->s.set_exact(enable != 0);
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_advance_info(mpfd_solver* h, mpfd_advance_info* out) {
+    return guard([&] {
+        if (!out) throw ConfigError("null argument");
+        out->iterations_run = h->s.last_iters;
+        out->wall_seconds = h->s.last_wall;
+        out->seconds_per_iteration = h->s.last_spi;
+        return MPFD_OK;
+    });
+}
+
+// memory_report (registry.cpp:24-39) over make_solver_fields' field set
+// (physics.cpp:441-475): Q, Qt, R and the five primitives always, the twelve
+// gradients for the Default strategy; every field ext^3 points
+int mpfd_b200_memory_census(mpfd_solver* h, mpfd_memory_census* out) {
+    return guard([&] {
+        if (!out) throw ConfigError("null argument");
+        Solver& S = h->s;
+        std::memset(out, 0, sizeof *out);
+        const size_t e = (size_t)S.n + 8;
+        const size_t pts = e * e * ((size_t)S.nzg + 8);
+        auto add = [&](int cls, const char* name) {
+            const size_t b = pts * byte_width(S.prec.resolve(cls, name));
+            out->count[cls] += 1;
+            out->bytes[cls] += b;
+            out->total_bytes += b;
+            out->baseline_b64_bytes += pts * 8;
+        };
+        for (int c = 0; c < 5; ++c) add(0, kQNames[c]);
+        for (int c = 0; c < 5; ++c) add(1, kTNames[c]);
+        for (int c = 0; c < 5; ++c) add(2, kRNames[c]);
+        for (int c = 0; c < 5; ++c) add(3, kPNames[c]);
+        if (S.strategy == MPFD_DEFAULT)
+            for (int i = 0; i < 12; ++i) add(3, kGNames[i]);
+        out->gain = out->total_bytes ? (double)out->baseline_b64_bytes / (double)out->total_bytes : 1.0;
+        for (auto& s : S.slabs) out->device_bytes += s.bytes;
         return MPFD_OK;
     });
 }
@@ -1522,6 +1760,7 @@ int mpfd_b200_set_path(mpfd_solver* h, int path) {
         Solver& S = h->s;
         if (path == 1 && !S.fused_ok) throw ConfigError("fused path not available for this precision plan");
         if (path != S.path) {
+            S.materialize_r();
             // move the state into the primary buffers before switching
             if (S.path == 1 && S.qbuf) {
                 for (auto& s : S.slabs) {
@@ -1529,7 +1768,7 @@ int mpfd_b200_set_path(mpfd_solver* h, int path) {
                     const size_t qel = (size_t)s.geo.planes * 5 * s.geo.plane * byte_width(S.plan.qk);
                     const size_t tel = (size_t)s.geo.nzl * 5 * s.geo.plane * byte_width(S.plan.tk);
                     CK(cudaMemcpyAsync(s.q, s.q2, qel, cudaMemcpyDeviceToDevice, s.stream));
-                    CK(cudaMemcpyAsync(s.qt, s.qt2, tel, cudaMemcpyDeviceToDevice, s.stream));
+                    if (S.exact && s.qt2) CK(cudaMemcpyAsync(s.qt, s.qt2, tel, cudaMemcpyDeviceToDevice, s.stream));
                 }
                 S.qbuf = 0;
             }

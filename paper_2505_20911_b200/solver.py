@@ -86,6 +86,16 @@ class _Step(C.Structure):
                 ("ke_weighting", C.c_int), ("threads", C.c_int)]
 
 
+class _AdvInfo(C.Structure):
+    _fields_ = [("iterations_run", C.c_long), ("wall_seconds", C.c_double),
+                ("seconds_per_iteration", C.c_double)]
+
+
+class _Census(C.Structure):
+    _fields_ = [("count", C.c_long * 5), ("bytes", C.c_size_t * 5), ("total_bytes", C.c_size_t),
+                ("baseline_b64_bytes", C.c_size_t), ("gain", C.c_double), ("device_bytes", C.c_size_t)]
+
+
 _lib = None
 
 
@@ -133,8 +143,20 @@ def lib():
                                        C.POINTER(C.c_size_t)]
         L.mpfd_b200_set_path.argtypes = [P, I]
         L.mpfd_b200_set_overlap.argtypes = [P, I]
+        L.mpfd_b200_set_exact_divergence.argtypes = [P, I]
+        L.mpfd_b200_advance_info.argtypes = [P, C.POINTER(_AdvInfo)]
+        L.mpfd_b200_memory_census.argtypes = [P, C.POINTER(_Census)]
+        L.mpfd_b200_issue_ceiling.argtypes = [I, C.POINTER(D)]
         _lib = L
     return _lib
+
+
+def issue_ceiling(device: int = 0) -> dict:
+    """Measured lane-op/s of unfused add/mul on `device`: fp64 (DADD/DMUL),
+    fp32 pairs (FADD2/FFMA2), fp16 pairs (HADD2/HMUL2)."""
+    out = (C.c_double * 3)()
+    _check(lib().mpfd_b200_issue_ceiling(device, out))
+    return {"fp64": out[0], "fp32": out[1], "fp16": out[2]}
 
 
 def _check(rc: int):
@@ -269,6 +291,8 @@ class AdvanceResult:
     divergence: Optional[DivergenceEvent]
     iterations_run: int
     series: List[DiagnosticsRecord]
+    wall_seconds: float = 0.0            # integrate.hpp:41-42
+    seconds_per_iteration: float = 0.0
 
 
 @dataclass
@@ -427,7 +451,10 @@ class Solver:
                                              C.byref(d), C.byref(it)))
         recs = [DiagnosticsRecord(x.t, x.kinetic_energy, x.enstrophy, x.eps_s, x.ke_normalized,
                                   bool(x.diverged)) for x in series[: ln.value]]
-        return AdvanceResult(rc == 2, _div(d) if rc == 2 else None, it.value, recs)
+        info = _AdvInfo()
+        _check(self.L.mpfd_b200_advance_info(self.h, C.byref(info)))
+        return AdvanceResult(rc == 2, _div(d) if rc == 2 else None, it.value, recs,
+                             info.wall_seconds, info.seconds_per_iteration)
 
     # --- measurement hooks --------------------------------------------------
     def run_steps(self, iters: int, dt: float, scheme: RKScheme = RKScheme()):
@@ -454,6 +481,21 @@ class Solver:
         a, b, c = C.c_size_t(), C.c_size_t(), C.c_size_t()
         _check(self.L.mpfd_b200_memory(self.h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
+
+    def memory_census(self) -> dict:
+        """memory_report (registry.cpp:24-39) of the reference's field set for
+        this config, plus the HBM this solver holds (device_bytes)."""
+        m = _Census()
+        _check(self.L.mpfd_b200_memory_census(self.h, C.byref(m)))
+        names = ("q_vector", "rk_arrays", "residuals", "wk_arrays", "diagnostics")
+        return {"per_class": {nm: {"count": m.count[i], "bytes": m.bytes[i]} for i, nm in enumerate(names)},
+                "total_bytes": m.total_bytes, "baseline_b64_bytes": m.baseline_b64_bytes,
+                "gain": m.gain, "device_bytes": m.device_bytes}
+
+    def set_exact_divergence(self, enable: bool):
+        """Exact divergence state: Qt and R double-buffered, slabs/ranks in
+        lock-step per substep (see mpfd_b200.h).  Default off."""
+        _check(self.L.mpfd_b200_set_exact_divergence(self.h, 1 if enable else 0))
 
     def halo_bytes(self) -> int:
         """Bytes this rank handed to ncclSend for halo exchanges so far."""

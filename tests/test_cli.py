@@ -17,7 +17,7 @@ def build_tool(b200):
     src = os.path.join(ROOT, "tools", "mpfd_b200_run.cpp")
     if not os.path.exists(TOOL) or os.path.getmtime(TOOL) < max(
             os.path.getmtime(src), os.path.getmtime(b200.library_path)):
-        subprocess.run(["g++", "-O2", "-std=c++17", "-I" + os.path.join(ROOT, "include"), src,
+        subprocess.run(["g++", "-O2", "-ffp-contract=off", "-std=c++17", "-I" + os.path.join(ROOT, "include"), src,
                         "-L" + os.path.dirname(b200.library_path), "-lmpfd_b200",
                         "-Wl,-rpath," + os.path.dirname(b200.library_path), "-o", TOOL], check=True)
     return TOOL

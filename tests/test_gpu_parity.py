@@ -6,6 +6,8 @@ equal to the reference after every substep, for every preset x emulation x
 strategy; diagnostics agree bitwise on bitwise-equal states (same reduction
 tree).  Checkers are run on the same seeded/deterministic inputs.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -166,11 +168,14 @@ def test_uniform_state_zero_residual(b200, preset):
             assert np.all(s.get_field(2, comp) == 0.0)
 
 
-@pytest.mark.parametrize("preset", ["DP", "HP"])
-def test_divergence_event(b200, preset):
-    """Inviscid Divergence split blows up: same event, iteration and series."""
+CODES = {"nonpositive or nonfinite density": 1, "nonfinite residual": 2, "nonfinite state": 3}
+
+
+def _divergence_run(b200, preset, exact, pz=1, path=None):
     kw = dict(preset=preset, split="Divergence", viscous=False, mach=0.4)
-    s = b200_solver(b200, 16, **kw)
+    s = b200_solver(b200, 16, decomp=b200.Decomposition(pz=pz) if pz > 1 else None, path=path, **kw)
+    if exact:
+        s.set_exact_divergence(True)
     c = checker(16, **kw)
     s.init_tgv()
     c.init()
@@ -178,13 +183,50 @@ def test_divergence_event(b200, preset):
     st, series, ev, it = c.advance(0.2, 400, 10)
     assert r.diverged and st == 2
     e = r.divergence
-    assert [{"nonpositive or nonfinite density": 1, "nonfinite residual": 2,
-             "nonfinite state": 3}[e.what], e.i, e.j, e.k, e.iteration, e.substep] == ev
+    assert [CODES[e.what], e.i, e.j, e.k, e.iteration, e.substep] == ev
     assert r.iterations_run == it
     got = np.array([[x.t, x.kinetic_energy, x.enstrophy, x.eps_s, x.diverged] for x in r.series])
     np.testing.assert_array_equal(np.isnan(got), np.isnan(series))
     assert same_bits(np.nan_to_num(got), np.nan_to_num(series))
-    assert_state(s, c, (0, 1), "divergence")
+    return s, c, CODES[e.what]
+
+
+@pytest.mark.parametrize("preset", ["DP", "HP"])
+def test_divergence_event(b200, preset):
+    """Inviscid Divergence split blows up: same event, iteration and series;
+    in exact-divergence mode Q, Qt and R at the event are the reference's."""
+    s, c, _ = _divergence_run(b200, preset, exact=True)
+    assert_state(s, c, (0, 1, 2), "divergence (exact)")
+
+
+@pytest.mark.parametrize("preset", ["DP", "HP"])
+def test_divergence_event_lean(b200, preset):
+    """Default (lean) layout -- Qt in place, R on demand: the event, the series
+    and Q are the reference's; Qt for a nonfinite-state event and R for
+    nonfinite-residual / nonfinite-state events too (mpfd_b200.h)."""
+    s, c, code = _divergence_run(b200, preset, exact=False)
+    assert_state(s, c, (0,), "divergence (lean) Q")
+    if code == 3:
+        assert_state(s, c, (1,), "divergence (lean) Qt")
+    if code in (2, 3):
+        assert_state(s, c, (2,), "divergence (lean) R")
+
+
+@pytest.mark.parametrize("pz", [2, 4])
+def test_divergence_event_slabs(b200, pz):
+    """Several z-slabs (overlapped exchange): the records of every slab merge
+    into the reference's first event; in exact mode the slabs run in
+    lock-step per substep and the whole state at the event is the
+    reference's."""
+    s, c, _ = _divergence_run(b200, "DP", exact=True, pz=pz)
+    assert_state(s, c, (0, 1, 2), f"divergence pz={pz} (exact)")
+    _divergence_run(b200, "DP", exact=False, pz=pz)
+
+
+def test_divergence_event_staged(b200):
+    """The staged (one kernel per level) path stops at the same event."""
+    s, c, _ = _divergence_run(b200, "DP", exact=False, path="staged")
+    assert_state(s, c, (0, 1, 2), "divergence (staged)")
 
 
 @pytest.mark.parametrize("pz", [2, 4])
@@ -339,6 +381,108 @@ def test_nccl_transport_single_rank(b200):
     rb = b.advance(b200.StepConfig(0.2, 400, 10))
     assert ra.diverged and rb.diverged and ra.divergence == rb.divergence
     assert ra.iterations_run == rb.iterations_run
+
+
+def _vs_reference(b200, n, preset, dt, steps, threads=None):
+    """advance `steps` RK steps on the fused path the bench times and on the
+    unmodified reference (oracle/_ref, all host threads); Q and Qt bit for bit."""
+    threads = threads or os.cpu_count() or 8
+    s = b200_solver(b200, n, preset)
+    s.init_tgv()
+    r = s.advance(b200.StepConfig(dt, steps, 0))
+    assert not r.diverged
+    c = checker(n, preset=preset, threads=threads)
+    c.init()
+    st, _, _, _ = c.advance(dt, steps, 0, threads=threads)
+    assert st == 0
+    for cls in (0, 1):
+        for comp in range(5):
+            g = s.get_field(cls, comp)
+            ref = c.field(cls, comp)
+            if not same_bits(g, ref):
+                bad = np.argwhere(g.view(np.uint64) != ref.view(np.uint64))
+                raise AssertionError(f"{n}^3 {preset} class {cls} comp {comp}: {len(bad)} mismatches")
+            del g, ref
+    s.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("preset", ["DP", "SPDP", "HPSP"])
+def test_256_cubed_step_vs_reference(b200, preset):
+    """BASELINE configs 2/3 (256^3 DP, SPDP; HPSP too): one RK step, bitwise
+    against the reference at the size the bench's per-precision lines run at
+    half scale (one step at 256^3)."""
+    _vs_reference(b200, 256, preset, 5e-4, 1)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("preset", ["DP", "SPDP", "HPSP"])
+def test_128_cubed_10_steps_vs_reference(b200, preset):
+    """128^3, 10 RK steps, bitwise against the reference."""
+    _vs_reference(b200, 128, preset, 1e-3, 10)
+
+
+@pytest.mark.slow
+def test_512_cubed_dp_step_vs_reference(b200):
+    """The bench's headline workload (TGV 512^3 DP, BASELINE.json metric): one
+    RK step, bitwise against the reference (22.5 GB of host carriers)."""
+    _vs_reference(b200, 512, "DP", 2.5e-4, 1)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("preset", ["DP", "SPDP", "HPSP"])
+def test_1024_cubed_fits_and_steps(b200, preset):
+    """BASELINE configs[4] size on ONE B200: Q (double-buffered) + Qt in HBM
+    (DP 129.9 GB), R and the diagnostics integrand never allocated; one RK
+    step; size-independent checks -- the state stays finite, K stays the
+    TGV's 1/8 to the decay of one step, and the solver holds exactly the
+    lean footprint."""
+    n = 1024
+    s = b200_solver(b200, n, preset)
+    bq, bt = {"DP": (8, 8), "SPDP": (8, 8), "HPSP": (4, 4)}[preset]
+    q_bytes = (n + 8) * 5 * n * n * bq
+    qt_bytes = 5 * n ** 3 * bt
+    dev = s.memory()[0]
+    assert 2 * q_bytes + qt_bytes <= dev <= 2 * q_bytes + qt_bytes + (1 << 30)
+    s.init_tgv()
+    d0 = s.diagnostics(0, 0.0, 8)
+    r = s.advance(b200.StepConfig(1.25e-4, 1, 1))
+    assert not r.diverged
+    k0, k1 = r.series[0].kinetic_energy, r.series[-1].kinetic_energy
+    assert k0 == d0.kinetic_energy and abs(k0 - 0.125) < 1e-6
+    assert 0 < k0 - k1 < 1e-6 and np.isfinite(r.series[-1].enstrophy)
+    assert s.memory()[0] == dev  # nothing allocated on the way
+    s.close()
+
+
+def test_lean_footprint_and_lazy_r(b200):
+    """The fused path holds Q twice and Qt once; R appears only when read,
+    bitwise the residual of the last substep's input; exact mode adds the
+    Qt and R double buffers and returns them when switched off."""
+    n = 32
+    s = b200_solver(b200, n, "DP")
+    c = checker(n, preset="DP")
+    q_bytes, qt_bytes = (n + 8) * 5 * n * n * 8, 5 * n ** 3 * 8
+    base = s.memory()[0]
+    assert 2 * q_bytes + qt_bytes <= base <= 2 * q_bytes + qt_bytes + (8 << 20)
+    s.init_tgv()
+    c.init()
+    assert np.all(s.get_field(2, 0) == 0.0) and s.memory()[0] == base
+    s.advance(b200.StepConfig(0.002, 2, 0))
+    c.advance(0.002, 2, 0)
+    assert_state(s, c, (0, 1, 2), "lazy R")
+    assert s.memory()[0] == base + qt_bytes  # R, allocated on the read
+    s.set_exact_divergence(True)
+    assert s.memory()[0] == base + 3 * qt_bytes
+    s.advance(b200.StepConfig(0.002, 1, 0))
+    c.advance(0.002, 1, 0)
+    assert_state(s, c, (0, 1, 2), "exact mode")
+    s.set_exact_divergence(False)
+    assert s.memory()[0] == base + qt_bytes
+    assert_state(s, c, (0, 1, 2), "exact mode off")
+    s.advance(b200.StepConfig(0.002, 1, 0))
+    c.advance(0.002, 1, 0)
+    assert_state(s, c, (0, 1, 2), "lean again")
 
 
 @pytest.mark.slow
