@@ -41,7 +41,7 @@ enum { MPFD_Q_VECTOR = 0, MPFD_RK_ARRAYS = 1, MPFD_RESIDUALS = 2, MPFD_WK_ARRAYS
 /* KeWeighting (tgv.hpp:24-27) */
 enum { MPFD_KE_PLAIN = 0, MPFD_KE_DENSITY = 1 };
 /* decomposition transport */
-enum { MPFD_DECOMP_LOCAL = 0, MPFD_DECOMP_NCCL = 1 };
+enum { MPFD_DECOMP_LOCAL = 0, MPFD_DECOMP_NCCL = 1, MPFD_DECOMP_IPC = 2 };
 
 /* GridSpec (field.hpp:20-56): cube n^3, spacing domain_length/n, halo 4.
  * z_periods > 1 (B200 extension for weak scaling, SURVEY.md 7 hard part 6)
@@ -76,10 +76,26 @@ typedef struct {
     double alpha, beta_rho, beta_u, beta_phi, gamma_rho, gamma_u, gamma_phi;
 } mpfd_split;
 
+/* Host all-gather supplied by the caller for MPFD_DECOMP_IPC (MPI_Allgather,
+ * torch.distributed on gloo, ...): every rank contributes `bytes` bytes from
+ * `send`; `recv` receives pz * bytes in rank order.  Host buffers; returns 0
+ * on success.  Called from the solver's control thread only, by every rank
+ * at the same points (it is also the solver's barrier). */
+typedef struct {
+    void* ctx;
+    int (*allgather)(void* ctx, const void* send, void* recv, size_t bytes);
+} mpfd_hostcomm;
+
 /* z-slab decomposition.  LOCAL: this process owns all pz slabs (one device
  * or `devices[pz]`), halos move by device copies.  NCCL: one slab per
  * process, `rank` of `pz`, communicator built from the 128-byte
- * ncclUniqueId in `nccl_id` (see mpfd_b200_nccl_unique_id). */
+ * ncclUniqueId in `nccl_id` (see mpfd_b200_nccl_unique_id); ghost planes
+ * move by ncclSend/ncclRecv.  IPC: one slab per process; the Q buffers are
+ * mapped into the neighbours with CUDA IPC and each rank PULLS its ghost
+ * planes with copy-engine transfers (cudaMemcpyAsync over NVLink, no SM
+ * work), ordered by epoch flags in device memory (stream wait/write-value
+ * operations); the small collectives (divergence keys, diagnostics
+ * partials) go through `hostcomm`. */
 typedef struct {
     int pz;
     int mode;
@@ -87,6 +103,7 @@ typedef struct {
     int device;
     const int* devices; /* LOCAL only; NULL -> all slabs on `device` */
     const void* nccl_id;
+    const mpfd_hostcomm* hostcomm; /* IPC only */
 } mpfd_decomp;
 
 /* DivergenceEvent (physics.hpp:85-91); code 1 "nonpositive or nonfinite
@@ -247,9 +264,32 @@ int mpfd_b200_halo_plan(int n, int pz, int rank, int bytes_q, long long out[9]);
  * under `prec`, per-name overrides first.  Pure host arithmetic: what the
  * reference's memory_report / comm_volume_report (registry.cpp:24-66) need. */
 int mpfd_b200_field_kind(const mpfd_precision* prec, int cls, const char* name, int* kind);
-/* Bytes this rank has handed to ncclSend for halo exchanges since creation
- * (the measured counterpart of comm_volume_report, registry.cpp:41-66). */
+/* Bytes of ghost planes this rank has moved since creation: handed to
+ * ncclSend (NCCL) or pulled by copy engines (IPC) -- the measured counterpart
+ * of comm_volume_report (registry.cpp:41-66). */
 int mpfd_b200_halo_bytes(mpfd_solver* s, unsigned long long* sent);
+
+/* The host merge steps of the distributed paths, the same functions the
+ * solver runs after its collectives; pure host arithmetic (no device), so the
+ * multi-rank logic can be driven on CPU (tests/test_decomp_gloo.py).
+ *
+ * Divergence: `count` per-slab / per-rank record tables of 15 words each,
+ * [code 0 density, 1 residual, 2 state][component], every word
+ * (key << 39) | global point index with key = 3 * iteration + substep, or
+ * UINT64_MAX for none.  Picks the earliest key and, inside it, the
+ * reference's check order (physics.cpp:573-584, integrate.cpp:135-147) and
+ * the first point in scan order (reduce.cpp:57-81) of an n x n x nz grid.
+ * Returns MPFD_DIVERGED with *ev filled, or MPFD_OK if no table holds a
+ * record. */
+int mpfd_b200_merge_divergence(const unsigned long long* tables, int count, int n, double dt,
+                               mpfd_divergence* ev);
+/* Diagnostics: the sum of deterministic_sum (reduce.cpp:14-36) over
+ * `npoints` integrand values, given `count` partials in global scan order:
+ * 4096-point chunk sums (chunked = 1; the slabs' chunks concatenated in z
+ * order) or the raw integrand (chunked = 0).  `threads` selects the
+ * reference's tree shape (1: pure pairwise; > 1: 4096-chunked). */
+int mpfd_b200_merge_diagnostics(const double* parts, size_t count, size_t npoints, int threads, int chunked,
+                                double* sum);
 
 /* Measured issue ceilings of the residual's arithmetic on `device` (SURVEY.md
  * 7 hard part 1), lane operations per second of unfused add/mul in the forms

@@ -13,6 +13,7 @@ from .solver import (  # noqa: F401
     ConfigError, DeviceError, DivergenceEvent, DiagnosticsRecord, AdvanceResult,
     FlowParams, GridSpec, PrecisionConfig, RKScheme, SplitCoefficients, StepConfig,
     Decomposition, Solver, lib, resolve_preset, split_preset, library_path, issue_ceiling,
+    LOCAL, NCCL, IPC, gloo_allgather, halo_plan, merge_divergence, merge_diagnostics,
 )
 
 __all__ = [
@@ -20,5 +21,6 @@ __all__ = [
     "ConfigError", "DeviceError", "DivergenceEvent", "DiagnosticsRecord", "AdvanceResult",
     "FlowParams", "GridSpec", "PrecisionConfig", "RKScheme", "SplitCoefficients",
     "StepConfig", "Decomposition", "Solver", "lib", "resolve_preset", "split_preset",
-    "library_path", "issue_ceiling",
+    "library_path", "issue_ceiling", "LOCAL", "NCCL", "IPC", "gloo_allgather", "halo_plan",
+    "merge_divergence", "merge_diagnostics",
 ]

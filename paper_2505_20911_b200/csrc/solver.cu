@@ -3,9 +3,10 @@
 //
 // One solver owns one or more z-slabs.  Each slab lives on one device with its
 // own stream and HBM arrays (kernels_staged.cuh has the layout).  Halos move
-// by device copies between slabs of this process (MPFD_DECOMP_LOCAL) or by
-// NCCL send/recv between processes (MPFD_DECOMP_NCCL, one slab per rank), in
-// the q_vector storage precision.
+// by device copies between slabs of this process (MPFD_DECOMP_LOCAL), by
+// NCCL send/recv between processes (MPFD_DECOMP_NCCL, one slab per rank), or
+// by copy-engine pulls from the neighbours' CUDA-IPC-mapped buffers
+// (MPFD_DECOMP_IPC), always in the q_vector storage precision.
 //
 // Reference interfaces replaced:
 //   make_solver_fields physics.cpp:441-475   -> Solver::Solver
@@ -147,6 +148,94 @@ static double tree_of_chunks(const double* c, size_t n) {
     return tree_of_chunks(c, h) + tree_of_chunks(c + h, n - h);
 }
 
+// deterministic_sum (reduce.cpp:14-36) of npoints integrand values from the
+// partials every slab / rank contributed, in global scan order: 4096-point
+// chunk sums (chunked) or the raw integrand
+static double merge_diag(const double* parts, size_t count, size_t N, int threads, bool chunked) {
+    if (chunked) {
+        if (N <= 4096) return parts[0];
+        if (threads > 1) return pairwise_sum(parts, count);
+        return tree_of_chunks(parts, count);  // count is a power of two here
+    }
+    if (threads > 1 && N > 4096) {
+        const size_t nch = (N + 4095) / 4096;
+        std::vector<double> c(nch);
+        for (size_t i = 0; i < nch; ++i)
+            c[i] = pairwise_sum(parts + i * 4096, std::min<size_t>(4096, N - i * 4096));
+        return pairwise_sum(c.data(), nch);
+    }
+    return pairwise_sum(parts, N);
+}
+
+// Merge per-slab (per-rank) divergence records into one DivergenceEvent: the
+// earliest substep any slab recorded, and inside it the reference's check
+// order -- density (primitives) -> nonfinite residual -> nonfinite state,
+// components in order, first point in scan order.  Every record carries its
+// key, so records of later substeps (a slab that ran ahead before it saw the
+// event) drop out of the minimum.
+static bool merge_div(const unsigned long long* tables, int count, int n, double dt, mpfd_divergence* ev) {
+    unsigned long long tot[15];
+    for (auto& v : tot) v = ULLONG_MAX;
+    for (int t = 0; t < count; ++t)
+        for (int i = 0; i < 15; ++i) tot[i] = std::min(tot[i], tables[t * 15 + i]);
+    unsigned long long best = ULLONG_MAX;
+    for (auto v : tot)
+        if (v != ULLONG_MAX) best = std::min(best, v >> kDivKeyShift);
+    if (best == ULLONG_MAX) return false;
+    const unsigned long long mask = (1ull << kDivKeyShift) - 1;
+    for (int code = 0; code < 3; ++code)
+        for (int comp = 0; comp < 5; ++comp) {
+            const unsigned long long v = tot[code * 5 + comp];
+            if (v == ULLONG_MAX || (v >> kDivKeyShift) != best) continue;
+            const unsigned long long gi = v & mask;
+            if (ev) {
+                const long iter = (long)(best / 3);
+                ev->code = code + 1;
+                ev->i = (int)(gi % (unsigned long long)n);
+                ev->j = (int)((gi / n) % (unsigned long long)n);
+                ev->k = (int)(gi / ((unsigned long long)n * n));
+                ev->iteration = iter;
+                ev->substep = (int)(best % 3);
+                ev->time = code == 2 ? (iter + 1) * dt : iter * dt;
+            }
+            return true;
+        }
+    return false;
+}
+
+// ---------------------------------------------------------------------------
+// CUDA driver stream memory operations (IPC transport), resolved through the
+// runtime so the library needs no -lcuda
+struct MemOps {
+    // cuStreamWaitValue32 / cuStreamWriteValue32 (CUresult, CUstream, CUdeviceptr, cuuint32_t, unsigned)
+    int (*wait32)(cudaStream_t, unsigned long long, unsigned, unsigned) = nullptr;
+    int (*write32)(cudaStream_t, unsigned long long, unsigned, unsigned) = nullptr;
+    static MemOps& get() {
+        static MemOps m;
+        if (!m.wait32) {
+            cudaDriverEntryPointQueryResult q;
+            void* f = nullptr;
+            if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess || !f)
+                throw DeviceError("cuStreamWaitValue32 unavailable");
+            m.wait32 = (int (*)(cudaStream_t, unsigned long long, unsigned, unsigned))f;
+            if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess || !f)
+                throw DeviceError("cuStreamWriteValue32 unavailable");
+            m.write32 = (int (*)(cudaStream_t, unsigned long long, unsigned, unsigned))f;
+        }
+        return m;
+    }
+    // CU_STREAM_WAIT_VALUE_GEQ = 0 ((int32)(*addr - v) >= 0); CU_STREAM_WRITE_VALUE_DEFAULT = 0
+    // (the write is ordered after the stream's prior work and its memory writes)
+    void wait_geq(cudaStream_t st, const unsigned* addr, unsigned v) const {
+        if (wait32(st, (unsigned long long)addr, v, 0) != 0) throw DeviceError("cuStreamWaitValue32 failed");
+    }
+    void write(cudaStream_t st, unsigned* addr, unsigned v) const {
+        if (write32(st, (unsigned long long)addr, v, 0) != 0) throw DeviceError("cuStreamWriteValue32 failed");
+    }
+};
+
 // ---------------------------------------------------------------------------
 struct Solver {
     unsigned long long halo_sent = 0;  // bytes handed to ncclSend by this rank
@@ -167,6 +256,26 @@ struct Solver {
     std::unique_ptr<Launcher> launch;
     std::vector<Slab> slabs;
     void* comm = nullptr;
+    // IPC transport (one slab per process): the caller's host all-gather,
+    // the neighbours' Q buffers and epoch flags mapped with CUDA IPC, and
+    // this rank's flags: [0] the epoch whose boundary planes are final,
+    // [1] / [2] the last epoch the lower / upper neighbour has pulled
+    mpfd_hostcomm hc{};
+    struct Peer {
+        int rank = -1;
+        void* q = nullptr;
+        void* q2 = nullptr;
+        unsigned* flags = nullptr;
+    };
+    Peer up_peer, dn_peer;
+    unsigned* flags = nullptr;
+    unsigned epoch = 0;
+    std::vector<void*> ipc_mapped;
+    bool dist() const { return mode != MPFD_DECOMP_LOCAL; }  // one slab per process
+    void host_allgather(const void* send, void* recv, size_t bytes);
+    void ipc_setup();
+    void ipc_pull(cudaStream_t main, cudaStream_t copy);
+    void ipc_wait_consumed(cudaStream_t st, unsigned e);
     int path = 1;  // 1 fused when available, 0 staged
     bool halo_fresh = false;
     int qbuf = 0;  // fused path: which Q buffer (and, exact mode, Qt buffer) holds the state
@@ -229,7 +338,7 @@ struct Solver {
     // pz == 1 in LOCAL mode (no neighbour) or slabs too thin to split
     int overlap = 1;
     bool overlap_ok() const {
-        return overlap && use_fused() && (pz > 1 || mode == MPFD_DECOMP_NCCL) && nzl() >= 3 * kHalo;
+        return overlap && use_fused() && (pz > 1 || dist()) && nzl() >= 3 * kHalo;
     }
     void exchange_async();
     void residual_enqueue(int iter, int sub);
@@ -246,6 +355,19 @@ struct Solver {
 };
 
 Solver::~Solver() {
+    if (mode == MPFD_DECOMP_IPC && hc.allgather) {
+        // neighbours may still read this rank's buffers: every rank drains
+        // its streams and passes the barrier before any memory is released
+        try {
+            sync();
+            std::vector<char> b((size_t)pz);
+            char me = 0;
+            host_allgather(&me, b.data(), 1);
+        } catch (...) {
+        }
+        for (void* p : ipc_mapped) cudaIpcCloseMemHandle(p);
+        cudaFree(flags);
+    }
     for (auto& s : slabs) {
         cudaSetDevice(s.device);
         for (void* p : {s.q, s.qt, s.r, s.q2, s.qt2, s.r2, s.prim, s.lev2}) cudaFree(p);
@@ -345,12 +467,14 @@ void Solver::setup(const mpfd_grid* grid, const mpfd_precision* p, int strategy_
     if (nzg % pz != 0) throw ConfigError("grid nz is not divisible by the z process count");
     if (nzg / pz < kHalo) throw ConfigError("z slab thinner than the halo depth (4)");
     const int nz_local = nzg / pz;
-    const int nslab = mode == MPFD_DECOMP_NCCL ? 1 : pz;
+    if (mode < MPFD_DECOMP_LOCAL || mode > MPFD_DECOMP_IPC) throw ConfigError("unknown decomposition mode");
+    if (dist() && (rank < 0 || rank >= pz)) throw ConfigError("rank out of range");
+    const int nslab = dist() ? 1 : pz;
     slabs.resize(nslab);
     for (int i = 0; i < nslab; ++i) {
         Slab& s = slabs[i];
         s.device = (mode == MPFD_DECOMP_LOCAL && d.devices) ? d.devices[i] : d.device;
-        const int r = mode == MPFD_DECOMP_NCCL ? rank : i;
+        const int r = dist() ? rank : i;
         s.geo.nx = n;
         s.geo.ny = n;
         s.geo.nzl = nz_local;
@@ -366,7 +490,108 @@ void Solver::setup(const mpfd_grid* grid, const mpfd_precision* p, int strategy_
         Nccl& nc = Nccl::get();
         nc.check(nc.commInitRank(&comm, pz, id, rank), "ncclCommInitRank");
     }
+    if (mode == MPFD_DECOMP_IPC) {
+        if (!d.hostcomm || !d.hostcomm->allgather) throw ConfigError("IPC decomposition needs hostcomm");
+        hc = *d.hostcomm;
+    }
     alloc();
+    if (mode == MPFD_DECOMP_IPC) ipc_setup();
+}
+
+void Solver::host_allgather(const void* send, void* recv, size_t bytes) {
+    if (hc.allgather(hc.ctx, send, recv, bytes) != 0) throw DeviceError("hostcomm allgather failed");
+}
+
+// Map the neighbours' Q buffers and flags into this process (CUDA IPC; on
+// peer devices the mapping enables NVLink peer access).  Every rank
+// publishes {q, q2, flags} handles through the host all-gather.
+void Solver::ipc_setup() {
+    Slab& s = slabs[0];
+    CK(cudaSetDevice(s.device));
+    CK(cudaMalloc(&flags, 4 * sizeof(unsigned)));
+    CK(cudaMemset(flags, 0, 4 * sizeof(unsigned)));
+    s.bytes += 4 * sizeof(unsigned);
+    MemOps::get();
+    CK(cudaDeviceSynchronize());
+    struct Handles {
+        cudaIpcMemHandle_t q, q2, f;
+        int has_q2;
+    } mine{};
+    CK(cudaIpcGetMemHandle(&mine.q, s.q));
+    if (s.q2) CK(cudaIpcGetMemHandle(&mine.q2, s.q2));
+    mine.has_q2 = s.q2 != nullptr;
+    CK(cudaIpcGetMemHandle(&mine.f, flags));
+    std::vector<Handles> all((size_t)pz);
+    host_allgather(&mine, all.data(), sizeof(Handles));
+    const int up = (rank + 1) % pz, dn = (rank + pz - 1) % pz;
+    auto open = [&](int r, Peer& p) {
+        p.rank = r;
+        if (r == rank) {  // pz == 1: this rank is its own neighbour
+            p.q = s.q;
+            p.q2 = s.q2;
+            p.flags = flags;
+            return;
+        }
+        auto map = [&](const cudaIpcMemHandle_t& h) {
+            void* ptr = nullptr;
+            CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+            ipc_mapped.push_back(ptr);
+            return ptr;
+        };
+        p.q = map(all[r].q);
+        p.q2 = all[r].has_q2 ? map(all[r].q2) : nullptr;
+        p.flags = (unsigned*)map(all[r].f);
+    };
+    open(dn, dn_peer);
+    if (up == dn) {
+        up_peer = dn_peer;  // pz == 2: one neighbour on both sides, mapped once
+        up_peer.rank = up;
+    } else {
+        open(up, up_peer);
+    }
+}
+
+// Ghost planes of the current state by copy-engine pulls from both
+// neighbours (fill_halos_periodic's z pass, field.cpp:29-36, distributed).
+// Epoch protocol, all on the GPU (no host sync, no SM):
+//   main stream:  flags[0] = e after the kernels that wrote this state
+//   copy stream:  wait dn.flags[0] >= e, up.flags[0] >= e; pull dn's top and
+//                 up's bottom H interior planes into the ghosts; tell each
+//                 neighbour it has been read (dn.flags[2] = e, up.flags[1] = e)
+// A producer overwrites a published buffer only after both neighbours have
+// pulled it (ipc_wait_consumed).
+void Solver::ipc_pull(cudaStream_t main, cudaStream_t copy) {
+    Slab& s = slabs[0];
+    const MemOps& mo = MemOps::get();
+    const size_t bq = byte_width(plan.qk);
+    const HaloPlan hp = halo_plan(n, nzg, pz, rank, (int)bq);
+    const unsigned e = ++epoch;
+    const bool alt = use_fused() && qbuf;
+    char* q = (char*)qcur(s);
+    const char* dq = (const char*)(alt ? dn_peer.q2 : dn_peer.q);
+    const char* uq = (const char*)(alt ? up_peer.q2 : up_peer.q);
+    mo.write(main, flags + 0, e);
+    if (copy != main) {
+        CK(cudaEventRecord(s.ev_b, main));
+        CK(cudaStreamWaitEvent(copy, s.ev_b, 0));
+    }
+    mo.wait_geq(copy, dn_peer.flags + 0, e);
+    mo.wait_geq(copy, up_peer.flags + 0, e);
+    // the neighbours' plans have the same offsets (equal slabs)
+    CK(cudaMemcpyAsync(q + hp.recv_lo, dq + hp.send_up, (size_t)hp.block, cudaMemcpyDeviceToDevice, copy));
+    CK(cudaMemcpyAsync(q + hp.recv_hi, uq + hp.send_dn, (size_t)hp.block, cudaMemcpyDeviceToDevice, copy));
+    mo.write(copy, dn_peer.flags + 2, e);
+    mo.write(copy, up_peer.flags + 1, e);
+    halo_sent += 2 * (unsigned long long)hp.block;
+}
+
+// before this rank overwrites the Q buffer that held epoch e: both
+// neighbours have pulled it
+void Solver::ipc_wait_consumed(cudaStream_t st, unsigned e) {
+    if (mode != MPFD_DECOMP_IPC || e == 0) return;
+    const MemOps& mo = MemOps::get();
+    mo.wait_geq(st, flags + 1, e);
+    mo.wait_geq(st, flags + 2, e);
 }
 
 void Solver::alloc() {
@@ -511,6 +736,21 @@ void Solver::set_exact(bool on) {
 // on every rank once any rank has diverged
 void Solver::substep_barrier() {
     if (!exact) return;
+    if (mode == MPFD_DECOMP_IPC) {
+        // host round trip per substep (exact mode is a diagnostic setting)
+        Slab& s = slabs[0];
+        CK(cudaSetDevice(s.device));
+        CK(cudaMemcpyAsync(pinned, &s.div->key, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s.stream));
+        CK(cudaStreamSynchronize(s.stream));
+        std::vector<unsigned long long> all((size_t)pz);
+        host_allgather(pinned, all.data(), sizeof(unsigned long long));
+        unsigned long long key = ULLONG_MAX;
+        for (auto v : all) key = std::min(key, v);
+        pinned[0] = key;
+        CK(cudaMemcpyAsync(&s.div->key, pinned, sizeof(unsigned long long), cudaMemcpyHostToDevice, s.stream));
+        CK(cudaStreamSynchronize(s.stream));
+        return;
+    }
     if (mode == MPFD_DECOMP_NCCL) {
         Slab& s = slabs[0];
         CK(cudaSetDevice(s.device));
@@ -656,6 +896,7 @@ void Solver::upload_planes(Slab& s, int cls, int comp, const double* src, size_t
     if (cls < 0 || cls > 2 || comp < 0 || comp > 4) throw ConfigError("bad class/component");
     const int kind = cls == 0 ? plan.qk : (cls == 1 ? plan.tk : plan.rk);
     CK(cudaSetDevice(s.device));
+    if (cls == 0) ipc_wait_consumed(s.stream, epoch);  // neighbours may still pull this buffer
     const long long pl = s.geo.plane;
     const int planes_per = (int)std::max<size_t>(1, s.staging_elems / pl);
     for (int z = zb; z < zb + nz; z += planes_per) {
@@ -816,6 +1057,13 @@ void Solver::init(int case_kind) {
 // H*5*ny*nx storage-precision values per direction.
 void Solver::halo_refresh() {
     const size_t bq = byte_width(plan.qk);
+    if (mode == MPFD_DECOMP_IPC) {
+        Slab& s = slabs[0];
+        CK(cudaSetDevice(s.device));
+        timed(2, s, [&] { ipc_pull(s.stream, s.stream); });
+        halo_fresh = true;
+        return;
+    }
     if (mode == MPFD_DECOMP_NCCL) {
         Slab& s = slabs[0];
         CK(cudaSetDevice(s.device));
@@ -910,6 +1158,14 @@ void Solver::exchange_async() {
     for (auto& s : slabs) {
         CK(cudaSetDevice(s.device));
         CK(cudaEventRecord(s.ev_b, s.stream));
+    }
+    if (mode == MPFD_DECOMP_IPC) {
+        Slab& s = slabs[0];
+        CK(cudaSetDevice(s.device));
+        ipc_pull(s.stream, s.comm);
+        ++prof_launch[2];
+        CK(cudaEventRecord(s.ev_x, s.comm));
+        return;
     }
     if (mode == MPFD_DECOMP_NCCL) {
         Slab& s = slabs[0];
@@ -1014,6 +1270,7 @@ void Solver::rk_enqueue(int sub, const double a[3], const double b[3], double dt
         view.q = qcur(s);
         view.qt = qtcur(s);
         view.r = rcur(s);
+        ipc_wait_consumed(s.stream, epoch);  // Q is updated in place
         timed(1, s, [&] { launch->rk(view, kc, iter, sub); });
         CK(cudaGetLastError());
     }
@@ -1061,12 +1318,16 @@ void Solver::substep_enqueue(int sub, const double a[3], const double b[3], doub
                               nz - kHalo);
             });
             if (need_x) CK(cudaStreamWaitEvent(s.stream, s.ev_x, 0));
+            // IPC: the neighbours pull the boundary planes of qout's previous
+            // state (epoch - 1) before the boundary launches overwrite them
+            ipc_wait_consumed(s.stream, epoch ? epoch - 1 : 0);
             timed(0, s, [&] {
                 launch->fused(s, qin, qout, qtin, qtout, rout, pc, rc, sc, staged, kc, write_r, iter, sub, 0, kHalo);
                 launch->fused(s, qin, qout, qtin, qtout, rout, pc, rc, sc, staged, kc, write_r, iter, sub,
                               nz - kHalo, nz);
             }, 2);
         } else {
+            ipc_wait_consumed(s.stream, epoch ? epoch - 1 : 0);
             timed(0, s, [&] {
                 launch->fused(s, qin, qout, qtin, qtout, rout, pc, rc, sc, staged, kc, write_r, iter, sub, 0, nz);
             });
@@ -1104,6 +1365,11 @@ bool Solver::poll_div(bool block) {
     }
     unsigned long long key = ULLONG_MAX;
     for (size_t i = 0; i < slabs.size(); ++i) key = std::min(key, pinned[i]);
+    if (mode == MPFD_DECOMP_IPC && block) {
+        std::vector<unsigned long long> all((size_t)pz);
+        host_allgather(&key, all.data(), sizeof key);
+        for (auto v : all) key = std::min(key, v);
+    }
     if (mode == MPFD_DECOMP_NCCL && block) {
         // every rank polls at the same iterations (the schedule is
         // deterministic), so this collective pairs up
@@ -1119,12 +1385,7 @@ bool Solver::poll_div(bool block) {
     return key != ULLONG_MAX;
 }
 
-// Merge the per-slab (per-rank) records into one DivergenceEvent: the
-// earliest substep any slab recorded, and inside it the reference's check
-// order -- density (primitives) -> nonfinite residual -> nonfinite state,
-// components in order, first point in scan order.  Records of later
-// substeps (a slab that ran ahead before it saw the event) carry a larger
-// key and drop out of the minimum.
+// the per-slab (per-rank) records, gathered, then merge_div
 bool Solver::resolve_div(mpfd_divergence* ev, double dt) {
     sync();
     unsigned long long tot[15];
@@ -1147,30 +1408,12 @@ bool Solver::resolve_div(mpfd_divergence* ev, double dt) {
         CK(cudaMemcpyAsync(pinned, s.red, sizeof tot, cudaMemcpyDeviceToHost, s.stream));
         CK(cudaStreamSynchronize(s.stream));
         std::memcpy(tot, pinned, sizeof tot);
+    } else if (mode == MPFD_DECOMP_IPC) {
+        std::vector<unsigned long long> all((size_t)pz * 15);
+        host_allgather(tot, all.data(), sizeof tot);
+        return merge_div(all.data(), pz, n, dt, ev);
     }
-    unsigned long long best = ULLONG_MAX;
-    for (auto v : tot)
-        if (v != ULLONG_MAX) best = std::min(best, v >> kDivKeyShift);
-    if (best == ULLONG_MAX) return false;
-    const unsigned long long mask = (1ull << kDivKeyShift) - 1;
-    for (int code = 0; code < 3; ++code)
-        for (int comp = 0; comp < 5; ++comp) {
-            const unsigned long long v = tot[code * 5 + comp];
-            if (v == ULLONG_MAX || (v >> kDivKeyShift) != best) continue;
-            const unsigned long long gi = v & mask;
-            if (ev) {
-                const long iter = (long)(best / 3);
-                ev->code = code + 1;
-                ev->i = (int)(gi % (unsigned long long)n);
-                ev->j = (int)((gi / n) % (unsigned long long)n);
-                ev->k = (int)(gi / ((unsigned long long)n * n));
-                ev->iteration = iter;
-                ev->substep = (int)(best % 3);
-                ev->time = code == 2 ? (iter + 1) * dt : iter * dt;
-            }
-            return true;
-        }
-    return false;
+    return merge_div(tot, 1, n, dt, ev);
 }
 
 // DiagnosticsComputer::compute (tgv.cpp:115-175) with the reference's
@@ -1225,21 +1468,13 @@ void Solver::diagnostics(int weighting, double t, int threads, mpfd_diag* out) {
             CK(cudaMemcpyAsync(parts.data() + o, src, cnt * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
             CK(cudaStreamSynchronize(s.stream));
         }
-        double sum;
-        if (aligned) {
-            const size_t nch = parts.size();
-            if (N <= 4096) sum = parts[0];
-            else if (threads > 1) sum = pairwise_sum(parts.data(), nch);
-            else sum = tree_of_chunks(parts.data(), nch);  // nch is a power of two here
-        } else if (threads > 1 && N > 4096) {
-            const size_t nch = (N + 4095) / 4096;
-            std::vector<double> c(nch);
-            for (size_t i = 0; i < nch; ++i)
-                c[i] = pairwise_sum(parts.data() + i * 4096, std::min<size_t>(4096, N - i * 4096));
-            sum = pairwise_sum(c.data(), nch);
-        } else {
-            sum = pairwise_sum(parts.data(), N);
+        if (mode == MPFD_DECOMP_IPC) {
+            // every rank's parts in rank (= global z) order
+            std::vector<double> all(parts.size() * pz);
+            host_allgather(parts.data(), all.data(), parts.size() * sizeof(double));
+            parts.swap(all);
         }
+        const double sum = merge_diag(parts.data(), parts.size(), N, threads, aligned);
         sums[which] = sum;
     }
     const double cell = h * h * h;
@@ -1466,7 +1701,7 @@ static void check_step(const mpfd_step* st) {
 // write_snapshot (io.cpp:69-85): int32 {n, n, n, 5}, then the five
 // conserved components as binary64, i fastest
 static void write_snapshot(Solver& S, const std::string& path) {
-    if (S.mode == MPFD_DECOMP_NCCL || S.zper != 1)
+    if (S.dist() || S.zper != 1)
         throw ConfigError("snapshots need the whole n^3 state in this process");
     std::FILE* f = std::fopen(path.c_str(), "wb");
     if (!f) throw ConfigError("cannot open for writing: " + path);
@@ -1524,7 +1759,7 @@ int mpfd_b200_advance(mpfd_solver* h, const mpfd_step* st, mpfd_diag* series, lo
         long done = 0;
         int status = MPFD_OK;
         mpfd_divergence e{};
-        const bool multi = S.mode == MPFD_DECOMP_NCCL;
+        const bool multi = S.dist();
         size_t next_snap = 0;
         for (long it = 0; it < st->n_iterations; ++it) {
             const bool last = it + 1 == st->n_iterations;
@@ -1734,6 +1969,28 @@ int mpfd_b200_halo_bytes(mpfd_solver* h, unsigned long long* sent) {
     return guard([&] {
         if (!sent) throw ConfigError("null argument");
         *sent = h->s.halo_sent;
+        return MPFD_OK;
+    });
+}
+
+int mpfd_b200_merge_divergence(const unsigned long long* tables, int count, int n, double dt,
+                               mpfd_divergence* ev) {
+    return guard([&] {
+        if (count < 0 || (count > 0 && !tables) || n < 1) throw ConfigError("bad divergence tables");
+        return merge_div(tables, count, n, dt, ev) ? MPFD_DIVERGED : MPFD_OK;
+    });
+}
+
+int mpfd_b200_merge_diagnostics(const double* parts, size_t count, size_t npoints, int threads, int chunked,
+                                double* sum) {
+    return guard([&] {
+        if (!parts || !sum || count == 0) throw ConfigError("bad diagnostics partials");
+        if (chunked ? count != (npoints + 4095) / 4096 : count != npoints)
+            throw ConfigError("partials do not match the point count");
+        if (chunked && npoints > 4096 && npoints % 4096 != 0) throw ConfigError("chunked partials need whole chunks");
+        if (chunked && threads <= 1 && (count & (count - 1)) != 0)
+            throw ConfigError("pure pairwise tree over chunk sums needs a power-of-two chunk count");
+        *sum = merge_diag(parts, count, npoints, threads, chunked != 0);
         return MPFD_OK;
     });
 }

@@ -65,9 +65,18 @@ class _Split(C.Structure):
                 ("alpha", "beta_rho", "beta_u", "beta_phi", "gamma_rho", "gamma_u", "gamma_phi")]
 
 
+# int (*allgather)(void* ctx, const void* send, void* recv, size_t bytes)
+_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+
+
+class _HostComm(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allgather", _ALLGATHER)]
+
+
 class _Decomp(C.Structure):
     _fields_ = [("pz", C.c_int), ("mode", C.c_int), ("rank", C.c_int), ("device", C.c_int),
-                ("devices", C.POINTER(C.c_int)), ("nccl_id", C.c_void_p)]
+                ("devices", C.POINTER(C.c_int)), ("nccl_id", C.c_void_p),
+                ("hostcomm", C.POINTER(_HostComm))]
 
 
 class _Div(C.Structure):
@@ -147,6 +156,9 @@ def lib():
         L.mpfd_b200_advance_info.argtypes = [P, C.POINTER(_AdvInfo)]
         L.mpfd_b200_memory_census.argtypes = [P, C.POINTER(_Census)]
         L.mpfd_b200_issue_ceiling.argtypes = [I, C.POINTER(D)]
+        L.mpfd_b200_halo_plan.argtypes = [I, I, I, I, C.POINTER(C.c_longlong)]
+        L.mpfd_b200_merge_divergence.argtypes = [C.POINTER(C.c_ulonglong), I, I, D, C.POINTER(_Div)]
+        L.mpfd_b200_merge_diagnostics.argtypes = [DP, C.c_size_t, C.c_size_t, I, I, DP]
         _lib = L
     return _lib
 
@@ -295,16 +307,65 @@ class AdvanceResult:
     seconds_per_iteration: float = 0.0
 
 
+LOCAL, NCCL, IPC = 0, 1, 2  # decomposition transports (mpfd_b200.h)
+
+
 @dataclass
 class Decomposition:
-    """z-slab decomposition: pz slabs, LOCAL (all slabs in this process) or
-    NCCL (one slab per rank, `nccl_id` from Solver.nccl_unique_id())."""
+    """z-slab decomposition: pz slabs, LOCAL (all slabs in this process),
+    NCCL (one slab per rank, `nccl_id` from Solver.nccl_unique_id()) or IPC
+    (one slab per rank, ghost planes pulled by copy engines from the
+    neighbours' CUDA-IPC-mapped buffers; `allgather(bytes) -> bytes` is the
+    host collective, every rank's contribution concatenated in rank order)."""
     pz: int = 1
-    mode: int = 0
+    mode: int = LOCAL
     rank: int = 0
     device: int = 0
     devices: Optional[List[int]] = None
     nccl_id: Optional[bytes] = None
+    allgather: Optional[object] = None
+
+
+def gloo_allgather(group=None):
+    """A Decomposition.allgather over torch.distributed (CPU tensors, e.g. the
+    gloo backend)."""
+    import torch
+    import torch.distributed as dist
+
+    def ag(data: bytes) -> bytes:
+        t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+        out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(out, t, group=group)
+        return b"".join(o.numpy().tobytes() for o in out)
+    return ag
+
+
+def halo_plan(n: int, pz: int, rank: int, bytes_q: int) -> dict:
+    """The z-slab halo plan the solver uses (mpfd_b200_halo_plan)."""
+    out = (C.c_longlong * 9)()
+    _check(lib().mpfd_b200_halo_plan(n, pz, rank, bytes_q, out))
+    keys = ("send_up", "recv_lo", "send_dn", "recv_hi", "block", "up", "dn", "z0", "nzl")
+    return dict(zip(keys, list(out)))
+
+
+def merge_divergence(tables: np.ndarray, n: int, dt: float) -> Optional["DivergenceEvent"]:
+    """The solver's merge of per-slab / per-rank divergence records
+    (mpfd_b200_merge_divergence): tables of shape (count, 15) uint64."""
+    t = np.ascontiguousarray(tables, dtype=np.uint64).reshape(-1, 15)
+    ev = _Div()
+    rc = _check(lib().mpfd_b200_merge_divergence(t.ctypes.data_as(C.POINTER(C.c_ulonglong)), t.shape[0], n,
+                                                  dt, C.byref(ev)))
+    return _div(ev) if rc == 2 else None
+
+
+def merge_diagnostics(parts: np.ndarray, npoints: int, threads: int, chunked: bool) -> float:
+    """The solver's host reduction of gathered diagnostics partials
+    (mpfd_b200_merge_diagnostics)."""
+    p = np.ascontiguousarray(parts, dtype=np.float64)
+    out = C.c_double()
+    _check(lib().mpfd_b200_merge_diagnostics(_dp(p), p.size, npoints, threads, 1 if chunked else 0,
+                                             C.byref(out)))
+    return out.value
 
 
 def _div(d: _Div) -> DivergenceEvent:
@@ -343,9 +404,23 @@ class Solver:
         d = decomp or Decomposition()
         self._devs = (C.c_int * max(1, len(d.devices or [])))(*(d.devices or [0]))
         self._nid = C.create_string_buffer(d.nccl_id, 128) if d.nccl_id else None
+        self._hc = None
+        if d.allgather is not None:
+            fn = d.allgather
+
+            def _ag(ctx, send, recv, nbytes):
+                try:
+                    out = fn(C.string_at(send, nbytes))
+                    C.memmove(recv, out, len(out))
+                    return 0
+                except Exception:  # reported to the solver as a failed collective
+                    return 1
+            self._agf = _ALLGATHER(_ag)  # kept alive with the solver
+            self._hc = _HostComm(None, self._agf)
         dd = _Decomp(d.pz, d.mode, d.rank, d.device,
                      self._devs if d.devices else None,
-                     C.cast(self._nid, C.c_void_p) if self._nid else None)
+                     C.cast(self._nid, C.c_void_p) if self._nid else None,
+                     C.pointer(self._hc) if self._hc is not None else None)
         self.h = C.c_void_p()
         _check(L.mpfd_b200_create(C.byref(g), C.byref(p), strategy, C.byref(f), C.byref(s),
                                   C.byref(dd), C.byref(self.h)))
@@ -498,7 +573,7 @@ class Solver:
         _check(self.L.mpfd_b200_set_exact_divergence(self.h, 1 if enable else 0))
 
     def halo_bytes(self) -> int:
-        """Bytes this rank handed to ncclSend for halo exchanges so far."""
+        """Bytes of ghost planes this rank moved so far (ncclSend or IPC pulls)."""
         v = C.c_ulonglong()
         _check(self.L.mpfd_b200_halo_bytes(self.h, C.byref(v)))
         return v.value
