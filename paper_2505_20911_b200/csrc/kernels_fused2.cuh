@@ -95,7 +95,9 @@ __device__ __forceinline__ RkIn2<QS, TS> rk_load2(const FusedArgs& a, int comp, 
     const long long ir = ((long long)c * 5 + comp) * a.g.plane + o;
     const long long iq = ((long long)(c + kHalo) * 5 + comp) * a.g.plane + o;
     RkIn2<QS, TS> v;
-    v.qt = a.kc.skip_a ? TS2() : __ldg(reinterpret_cast<const TS2*>((const TS*)a.qtin + ir));
+    // Qt is updated in place by this thread later in the kernel: a coherent
+    // load that bypasses L1 (ld.global.cg), not the read-only path
+    v.qt = a.kc.skip_a ? TS2() : __ldcg(reinterpret_cast<const TS2*>((const TS*)a.qtin + ir));
     v.q = __ldg(reinterpret_cast<const QS2*>((const QS*)a.qin + iq));
     return v;
 }
@@ -587,30 +589,55 @@ struct FusedPlan {
 #ifndef MPFD_WS_STAGE
 #define MPFD_WS_STAGE 1
 #endif
-    using TLW = typename std::conditional<sizeof(T) == 2, TileWS<64, MPFD_WS_TY, MPFD_WS_NR, MPFD_WS_STAGE != 0>,
-                                          TileWS<32, MPFD_WS32_TY, 6, MPFD_WS32_STAGE != 0>>::type;
+#ifndef MPFD_WS_TMA
+#define MPFD_WS_TMA 1
+#endif
+    // fp16 compute stages Q by TMA where the geometry allows (tma_ok), else
+    // by cp.async (TLWC)
+    using TLWC = typename std::conditional<sizeof(T) == 2, TileWS<64, MPFD_WS_TY, MPFD_WS_NR, MPFD_WS_STAGE != 0>,
+                                           TileWS<32, MPFD_WS32_TY, 6, MPFD_WS32_STAGE != 0>>::type;
+    using TLW = typename std::conditional<
+        sizeof(T) == 2, TileWS<64, MPFD_WS_TY, MPFD_WS_NR, MPFD_WS_STAGE != 0, MPFD_WS_TMA != 0>, TLWC>::type;
     static constexpr int NPW = sizeof(T) == 2 ? MPFD_WS_NPW : MPFD_WS32_NPW;
     static constexpr bool WS = MPFD_WS != 0 && PAIR && (sizeof(T) == 2 || MPFD_WS32 != 0) &&
-                               WsSmem<TLW, T, PT, QS>::total <= 232448;
+                               WsSmem<TLW, T, PT, QS>::total <= 232448 && WsSmem<TLWC, T, PT, QS>::total <= 232448;
+
+    template <class TLx, bool ST, unsigned SPL>
+    static void go_ws(FusedArgs a, cudaStream_t st, const WsTma& tm) {
+        auto kern = k_fused_ws<QS, TS, RS, PT, WC, T, TC, QC, ST, TLx, NPW, SPL>;
+        constexpr size_t smem = WsSmem<TLx, T, PT, QS>::total;
+        static unsigned done = 0;
+        static int ok = -1;
+        smem_optin(kern, smem, done);
+        if (ok < 0) {
+            cudaFuncAttributes fa{};
+            ok = cudaFuncGetAttributes(&fa, kern) == cudaSuccess && WsRegs<T, TLx, NPW>::fits(fa.numRegs);
+        }
+        if (!ok) throw std::runtime_error("warp-specialised kernel: register split exceeds the launch pool");
+        a.lz = z_range(a.g, a.zhi - a.zlo, TLx::TX, TLx::TY, 1);
+        const dim3 grid((a.g.nx + TLx::TX - 1) / TLx::TX, (a.g.ny + TLx::TY - 1) / TLx::TY,
+                        (a.zhi - a.zlo + a.lz - 1) / a.lz);
+        kern<<<grid, NPW * 32 + TLx::NT / 2, smem, st>>>(a, tm);
+    }
+    // TMA staging needs every box of the R4 box contiguous after wrapping:
+    // whole tiles in x, 4-row groups in y (tma.cuh)
+    static bool tma_ok(const Geo& g) {
+        return g.nx % TLW::TX == 0 && g.ny % 4 == 0 && ((size_t)g.nx * sizeof(QS)) % 16 == 0;
+    }
 
     template <bool ST, unsigned SPL>
     static void go(FusedArgs a, cudaStream_t st) {
         if constexpr (WS) {
             if (a.g.nx % 2 == 0) {
-                auto kern = k_fused_ws<QS, TS, RS, PT, WC, T, TC, QC, ST, TLW, NPW, SPL>;
-                constexpr size_t smem = WsSmem<TLW, T, PT, QS>::total;
-                static unsigned done = 0;
-                static int ok = -1;
-                smem_optin(kern, smem, done);
-                if (ok < 0) {
-                    cudaFuncAttributes fa{};
-                    ok = cudaFuncGetAttributes(&fa, kern) == cudaSuccess && WsRegs<T, TLW, NPW>::fits(fa.numRegs);
+                static const WsTma none{};
+                if constexpr (TLW::TMA) {
+                    if (tma_ok(a.g)) {
+                        go_ws<TLW, ST, SPL>(a, st,
+                                            ws_tma_maps<QS>(a.qin, a.g.nx, a.g.ny, a.g.planes, TLW::TX, TLW::TY));
+                        return;
+                    }
                 }
-                if (!ok) throw std::runtime_error("warp-specialised kernel: register split exceeds the launch pool");
-                a.lz = z_range(a.g, a.zhi - a.zlo, TLW::TX, TLW::TY, 1);
-                const dim3 grid((a.g.nx + TLW::TX - 1) / TLW::TX, (a.g.ny + TLW::TY - 1) / TLW::TY,
-                                (a.zhi - a.zlo + a.lz - 1) / a.lz);
-                kern<<<grid, NPW * 32 + TLW::NT / 2, smem, st>>>(a);
+                go_ws<TLWC, ST, SPL>(a, st, none);
                 return;
             }
         }

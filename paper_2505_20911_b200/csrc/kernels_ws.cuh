@@ -28,17 +28,21 @@
 #pragma once
 
 #include "kernels_fused2.cuh"
+#include "tma.cuh"
 
 namespace mpfd_b200 {
 
 // NR ring slots (>= 6): A(p) may run NR-6 planes further ahead of the
 // residual; the level-2 buffer then needs NR-4 planes and each hand-off kind
 // NB = NR-4 barrier ids (planes whose hand-off can be outstanding at once)
-template <int TX_, int TY_, int NR = 6, bool STG = true>
+template <int TX_, int TY_, int NR = 6, bool STG = true, bool TMA_ = false>
 struct TileWS {
-    // STG: next plane's Q staged by cp.async; otherwise producers load it
-    // from global memory, prefetched into L2 two planes ahead
+    // STG: next plane's Q staged in shared memory -- by TMA (TMA_: one
+    // elected producer thread, tma.cuh) or by every producer thread's
+    // cp.async; otherwise producers load it from global memory, prefetched
+    // into L2 two planes ahead
     static constexpr bool STAGE = STG;
+    static constexpr bool TMA = STG && TMA_;
     static constexpr int TX = TX_, TY = TY_, NT = TX * TY;
     static constexpr int R4X = TX + 8, R4Y = TY + 8, R4N = R4X * R4Y;
     static constexpr int R2X = TX + 4, R2Y = TY + 4, R2N = R2X * R2Y;
@@ -58,8 +62,13 @@ struct WsSmem {
     static constexpr size_t pp_bytes = (size_t)TL::NRING * TL::R2N * sizeof(PT);
     static constexpr size_t q_bytes = (size_t)5 * TL::NRING * TL::R2N * sizeof(RCt);
     static constexpr size_t l_bytes = (size_t)TL::LBD * 5 * TL::R2N * sizeof(RCt);
-    static constexpr size_t s_off = (p_bytes + pp_bytes + q_bytes + l_bytes + 15) & ~(size_t)15;
-    static constexpr size_t total = s_off + (TL::STAGE ? (size_t)5 * TL::R4N * sizeof(QS) : 0);
+    // TMA: four mbarriers (staging full / consumed, per buffer), then two
+    // staging buffers of 128-byte aligned parts
+    static constexpr size_t mb_off = (p_bytes + pp_bytes + q_bytes + l_bytes + 15) & ~(size_t)15;
+    static constexpr size_t s_off = TL::TMA ? (mb_off + 32 + 127) & ~(size_t)127 : mb_off;
+    static constexpr size_t s_bytes =
+        TL::TMA ? 2 * WsParts<TL::TX, TL::TY, QS>::total : (TL::STAGE ? (size_t)5 * TL::R4N * sizeof(QS) : 0);
+    static constexpr size_t total = s_off + s_bytes;
 };
 
 __device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -103,7 +112,8 @@ struct WsRegs {
 
 template <class QS, class TS, class RS, class PT, class WC, class T, class TC, class QC, bool STAGED, class TL,
           int NPW, unsigned SPL>
-__global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs a) {
+__global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1)
+    k_fused_ws(FusedArgs a, const __grid_constant__ WsTma tm) {
     if (a.div->key < div_key(a.iter, a.sub)) return;
     using T2 = typename V2<T>::type;
     using WC2 = typename V2<WC>::type;
@@ -123,6 +133,10 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
     T* Qr = (T*)(smem_raw + SM::p_bytes + SM::pp_bytes);
     T* Lbuf = (T*)(smem_raw + SM::p_bytes + SM::pp_bytes + SM::q_bytes);
     QS* Sg = (QS*)(smem_raw + SM::s_off);
+    // TMA staging, buffer b: mb[b] full (transaction count), mb[2 + b]
+    // consumed (NP arrivals)
+    unsigned long long* mb = (unsigned long long*)(smem_raw + SM::mb_off);
+    using PARTS = WsParts<TL::TX, TL::TY, QS>;
 
     const Geo& g = a.g;
     const int tid = threadIdx.x;
@@ -141,10 +155,17 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
     // phase A of one point pair: staging pair index si, rim descriptor ri
     // (element index | R2 index << 13 | in R2 << 26 | owned interior << 27),
     // wrapped in-plane offset roff; copies plane p+1 into its staging entries
+    // si: staging pair index (cp.async layout [5][R4N]) or, with TMA, the
+    // element offset in the staging parts | component stride << 16
     auto a_pair = [&](int p, int si, unsigned ri, int roff) {
         const int slot = TL::slot(p);
         QS2 q0, q1, q2, q3, q4;
-        if constexpr (TL::STAGE) {
+        if constexpr (TL::TMA) {
+            const QS* sp = Sg + (si & 0xFFFF);
+            const int cs = si >> 16;
+            q0 = ldv<QS>(sp), q1 = ldv<QS>(sp + cs), q2 = ldv<QS>(sp + 2 * cs), q3 = ldv<QS>(sp + 3 * cs),
+            q4 = ldv<QS>(sp + 4 * cs);
+        } else if constexpr (TL::STAGE) {
             const QS* sp = Sg + 2 * si;
             q0 = ldv<QS>(sp), q1 = ldv<QS>(sp + TL::R4N), q2 = ldv<QS>(sp + 2 * TL::R4N),
             q3 = ldv<QS>(sp + 3 * TL::R4N), q4 = ldv<QS>(sp + 4 * TL::R4N);
@@ -167,7 +188,7 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
         const WC2 rho = cvt<WC2>(q0);
         const PrimOut<WC2> pv =
             PrimCalc<WC2>::run(rho, cvt<WC2>(q1), cvt<WC2>(q2), cvt<WC2>(q3), cvt<WC2>(q4), half, gm1, gM2);
-        if (TL::STAGE && p + 1 < ze + 4) {
+        if (TL::STAGE && !TL::TMA && p + 1 < ze + 4) {
             // this thread's staging entries were consumed (their loads fed the
             // primitives above): copy plane p+1 into them
             const QS* qb = qin + (long long)(p + 1 + kHalo) * 5 * g.plane + roff;
@@ -271,6 +292,18 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
     // (SPDP), fp16 14.5 -> 15.5 ms (HPSP), so fp32 only
     constexpr bool CRIM = MPFD_WS_CRIM != 0 && sizeof(T) == 4;
 
+    if constexpr (TL::TMA) {
+        if (tid == 0) {
+            mbar_init(mb, 1);
+            mbar_init(mb + 1, 1);
+            mbar_init(mb + 2, NP);
+            mbar_init(mb + 3, NP);
+            mbar_fence_init();
+            tma_prefetch_desc(&tm.map[0]);
+            tma_prefetch_desc(&tm.map[1]);
+        }
+        __syncthreads();
+    }
     if (tid < NP) {
         // ======================= producers ====================================
         if constexpr (PREG > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PREG));
@@ -285,11 +318,44 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
             const int j = min(ptid + k * NP, NRIM - 1);
             const int ry = j / R4P, pc = j - ry * R4P;
             rsi[k] = ry * R4P + pc;
+            if constexpr (TL::TMA) {
+                // part of x = 2 pc (low rim, centre, high rim), 4-row group of ry
+                const int rx = 2 * pc;
+                const int xp = rx < 4 ? 0 : (rx < TL::TX + 4 ? 1 : 2);
+                const int xin = xp == 0 ? rx : (xp == 1 ? rx - 4 : rx - TL::TX - 4);
+                const int w = PARTS::w(xp);
+                const int off = PARTS::offset(xp) + (ry >> 2) * PARTS::gstride(xp) + (ry & 3) * w + xin;
+                rsi[k] = off | ((4 * w) << 16);
+            }
             rim_off[k] = wrap_off(2 * pc, ry);
             rinfo[k] = rim_desc(2 * pc, ry);
         }
+        // TMA: the elected thread moves plane p's R4 box (all five
+        // components) into staging buffer b, completing on mb[b]
+        constexpr int SBUF = (int)(PARTS::total / sizeof(QS));
+        auto tma_issue = [&](int p, int b) {
+            mbar_expect_tx(mb + b, PARTS::tx_bytes);
+            const int xs[3] = {x0 - 4 < 0 ? g.nx - 4 : x0 - 4, x0, x0 + TL::TX >= g.nx ? x0 + TL::TX - g.nx : x0 + TL::TX};
+            const int zc = p + kHalo;
+#pragma unroll
+            for (int gy = 0; gy < PARTS::NG; ++gy) {
+                int yy = y0 - 4 + 4 * gy;
+                yy += yy < 0 ? g.ny : 0;
+                yy -= yy >= g.ny ? g.ny : 0;
+#pragma unroll
+                for (int xp = 0; xp < 3; ++xp)
+                    tma_load4(Sg + b * SBUF + PARTS::offset(xp) + gy * PARTS::gstride(xp), &tm.map[xp == 1 ? 1 : 0],
+                              xs[xp], yy, 0, zc, mb + b);
+            }
+        };
+        if constexpr (TL::TMA) {
+            if (ptid == 0) {
+                tma_issue(zs - 4, 0);
+                if (zs - 3 < ze + 4) tma_issue(zs - 3, 1);
+            }
+        }
         // each producer thread copies exactly the staging entries it reads
-        if constexpr (TL::STAGE) {
+        if constexpr (TL::STAGE && !TL::TMA) {
             const QS* qb = qin + (long long)(zs - 4 + kHalo) * 5 * g.plane;
 #pragma unroll
             for (int k = 0; k < KPF; ++k) {
@@ -305,13 +371,29 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1) k_fused_ws(FusedArgs
             // A(p) overwrites the slot of plane p-6 (last read by C(p-4)); the
             // rim part of B(p-2) below overwrites the level-2 buffer of p-4
             if (p >= zs + TL::NRING - 4) nb_sync(TL::bid(BAR::EMPTY, p), NALL);
-            cp_async_wait_all();
+            // TMA: plane k = p - (zs - 4) sits in buffer k & 1, fill (k >> 1)
+            const int kk = p - (zs - 4);
+            const int sb = kk & 1;
+            const unsigned ph = (unsigned)(kk >> 1) & 1u;
+            if constexpr (TL::TMA) {
+                // stage plane p+1 into the buffer plane p-1 used, once every
+                // producer has read it
+                if (ptid == 0 && kk >= 1 && p + 1 < ze + 4) {
+                    mbar_wait(mb + 2 + (sb ^ 1), (unsigned)((kk - 1) >> 1) & 1u);
+                    tma_issue(p + 1, sb ^ 1);
+                }
+                mbar_wait(mb + sb, ph);  // plane p staged
+            } else {
+                cp_async_wait_all();
+            }
+            const int soff = TL::TMA ? sb * SBUF : 0;
 #pragma unroll
             for (int k = 0; k < KPF; ++k) {
                 if (ptid + k * NP >= NRIM) break;
-                a_pair(p, rsi[k], rinfo[k], rim_off[k]);
+                a_pair(p, rsi[k] + soff, rinfo[k], rim_off[k]);
             }
-            cp_async_commit();
+            if constexpr (TL::TMA) mbar_arrive(mb + 2 + sb);  // this producer has read plane p
+            else cp_async_commit();
             if (p >= zs) nb_arrive(TL::bid(BAR::FULL, p), NALL);
             // ---- rim part of B(p-2): needs A(p) of every producer ----
             const int cpl = p - 2;
