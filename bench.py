@@ -217,6 +217,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nccl", action="store_true",
                     help="use the NCCL transport even on one rank (self-exchange)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
+                    help="halo transport between ranks: ncclSend/Recv, or copy-engine pulls from "
+                         "CUDA-IPC-mapped neighbour buffers (host collectives over gloo)")
+    ap.add_argument("--no-memory-table", action="store_true",
+                    help="skip the measured per-preset memory table (Default strategy, materialised)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-overlap", action="store_true",
                     help="exchange ghost planes before the substep instead of overlapping")
@@ -240,6 +245,7 @@ def main():
             os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
                               MASTER_PORT=os.environ.get("MASTER_PORT", "29533"))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    gloo = dist.new_group(backend="gloo") if use_nccl and args.transport == "ipc" else None
     hbm, peak_src = peaks()
     try:
         ceil = m.issue_ceiling(local)
@@ -251,7 +257,10 @@ def main():
         dt = DT.get(n, 2.5e-4)
         prec = m.resolve_preset(preset, args.emulation)
         decomp = None
-        if use_nccl:
+        if use_nccl and args.transport == "ipc":
+            decomp = m.Decomposition(pz=world, mode=m.IPC, rank=rank, device=local,
+                                     allgather=m.gloo_allgather(gloo))
+        elif use_nccl:
             obj = [m.Solver.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
             decomp = m.Decomposition(pz=world, mode=1, rank=rank, device=local, nccl_id=obj[0])
@@ -378,7 +387,8 @@ def main():
                                        f"{args.grid * world} stacked periods)"
                                        if args.scaling == "weak" and world > 1 else "")),
                        "n": args.grid, "precision": args.precision, "path": head["path"],
-                       "decomposition": f"z-slabs x{world}" + (" (NCCL)" if use_nccl else ""),
+                       "decomposition": f"z-slabs x{world}" + ((" (IPC copy engines)" if args.transport == "ipc"
+                                                                  else " (NCCL)") if use_nccl else ""),
                        "halo_exchange": ("overlapped with interior planes (2 streams)"
                                          if use_nccl and not args.no_overlap else
                                          "before each substep" if use_nccl else
@@ -399,6 +409,8 @@ def main():
         }
         if "e2e" in head:
             line["e2e"] = head["e2e"]
+        if not args.no_memory_table and world == 1:
+            line["memory_table"] = memory_table(m, args, local)
         if "halo" in head:
             line["halo"] = head["halo"]
         if not args.no_cpu_baseline and world == 1:
@@ -416,6 +428,41 @@ def main():
     if use_nccl:
         dist.destroy_process_group()
     return 0
+
+
+def memory_table(m, args, device):
+    """The paper's memory table measured: per preset, the
+    HBM the solver holds against the reference's analytic census of the same
+    field set (memory_report, registry.cpp:24-39), for the Default strategy
+    on the materialised path (the reference's dataflow: the 12 ddx1-staged
+    gradients held at wk storage, plus primitives and level-2 fields) and
+    for Storesome on the fused path the bench times (primitives, gradients
+    and level-2 fields never reach HBM).  Allocation only: one residual
+    evaluation on a uniform state allocates the staged arrays."""
+    out = {}
+    for preset in ("DP", "SPDP", "HPSP"):
+        row = {}
+        for strategy, path in (("default", "materialised"), ("storesome", "fused")):
+            try:
+                s = m.Solver(m.GridSpec(args.grid), m.resolve_preset(preset, args.emulation), strategy,
+                             m.FlowParams(0.1, 1600.0, 0.72, 1.4, True), args.split, m.Decomposition(device=device))
+                s.set_path(path)
+                s.init_uniform()
+                if path == "materialised":
+                    s.evaluate()
+                mc = s.memory_census()
+                row[f"{strategy}/{path}"] = {"device_bytes": mc["device_bytes"], "census_bytes": mc["total_bytes"],
+                                             "census_b64_bytes": mc["baseline_b64_bytes"],
+                                             "census_gain": mc["gain"],
+                                             "device_over_census": mc["device_bytes"] / mc["total_bytes"]}
+                s.close()
+            except Exception as e:  # report, never hide
+                row[f"{strategy}/{path}"] = {"error": str(e)}
+        out[preset] = row
+    out["note"] = (f"{args.grid}^3; device_bytes = HBM held (Q double-buffered on the fused path, "
+                   "staged arrays with ghost planes on the materialised path); census = the "
+                   "reference's memory_report for the same field set, halos included")
+    return out
 
 
 PIPE = {8: "fp64 (DADD/DMUL)", 4: "fp32 pairs (FADD2/FFMA2)", 2: "fp16 pairs (HADD2/HMUL2)"}
@@ -437,16 +484,24 @@ def compute_roofline(preset, npts, avg_ms, ceil):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_ops.json")) as f:
             d = json.load(f)
-        ops = d.get(f"{preset}/fused/ops_per_pt")
-        pct = d.get(f"{preset}/fused/pipe_active_pct")
     except Exception:
-        ops = pct = None
+        d = {}
+    ops = d.get(f"{preset}/fused/ops_per_pt")
+    pct = d.get(f"{preset}/fused/pipe_active_pct")
     if ops:
         out["ops_per_pt_per_launch"] = ops
         out["achieved_gops"] = ops * npts / (avg_ms * 1e-3) / 1e9
         if out["ceiling_gops"]:
             out["frac"] = out["achieved_gops"] / out["ceiling_gops"]
     out["ncu_pipe_active_pct"] = pct
+    issue = d.get(f"{preset}/fused/issue_active_pct")
+    stalls = d.get(f"{preset}/fused/top_stalls")
+    if issue is not None:
+        # what bounds the kernel, from the committed capture: the HBM
+        # fraction above is far from 1, so it is the instruction stream
+        out["limiter"] = (f"issue/latency: issue {issue}% of peak, {PIPE[rb].split()[0]} pipe {pct}% active, "
+                          f"warps {d.get(f'{preset}/fused/warps_active_pct')}% of max; top stalls "
+                          + ", ".join(f"{a} {b}" for a, b in (stalls or [])[:3]))
     return out
 
 

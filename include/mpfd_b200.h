@@ -297,7 +297,11 @@ int mpfd_b200_merge_diagnostics(const double* parts, size_t count, size_t npoint
  * FFMA2 with an opaque zero), out[2] fp16 pairs (HADD2/HMUL2). */
 int mpfd_b200_issue_ceiling(int device, double out[3]);
 
-/* Which residual path runs: 0 = staged multi-kernel, 1 = fused. */
+/* Which residual path runs: 0 = staged multi-kernel, 1 = fused (default),
+ * 2 = staged with the Default strategy's ddx1 staging materialised: the 12
+ * gradient arrays (make_solver_fields physics.cpp:463-473, filled by
+ * stencil.cpp:11-28 at physics.cpp:503-517) held in HBM at their wk storage,
+ * as the reference holds them.  Bitwise the same results on every path. */
 int mpfd_b200_set_path(mpfd_solver* s, int path);
 /* Overlap of the z-halo exchange with the interior planes (fused path,
  * pz > 1 or NCCL): 1 (default) splits each substep into the interior

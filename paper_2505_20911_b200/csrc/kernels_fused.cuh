@@ -175,6 +175,7 @@ __device__ __forceinline__ RkIn<QS, TS> rk_load(const FusedArgs& a, int comp, in
     const long long ir = ((long long)c * 5 + comp) * a.g.plane + o;
     const long long iq = ((long long)(c + kHalo) * 5 + comp) * a.g.plane + o;
     RkIn<QS, TS> v;
+    // in-place Qt through the read-only path: see rk_load2
     v.qt = a.kc.skip_a ? TS() : __ldg((const TS*)a.qtin + ir);
     v.q = __ldg((const QS*)a.qin + iq);
     return v;

@@ -1,6 +1,7 @@
 // kernels_staged.cuh -- the staged residual path (one kernel per level).
 //
 //   k_prim   primitives_impl        physics.cpp:281-331 (all Q planes, incl. ghosts)
+//   k_grad   ddx1 staging           stencil.cpp:11-28 (Default, materialised)
 //   k_level2 divu / sum u tau / dT   physics.cpp:217-271 (+ ddx1 staging for
 //                                    the Default strategy, stencil.cpp:11-28)
 //   k_resid  residual_slab          physics.cpp:345-394 + finite scan :573-584
@@ -15,6 +16,7 @@
 //   Qt,R [nzl][5][ny][nx]
 //   prim [5 field][nzl+2H][ny][nx]   (staged path only)
 //   lev2 [7 field][nzl+2H][ny][nx]   (staged path only)
+//   grad [12 field][nzl+2H][ny][nx]  (materialised Default path only)
 #pragma once
 
 #include "stencil.cuh"
@@ -168,12 +170,42 @@ struct StageConsts {
     int kind[12];    // storage kinds of dudx..dwdz, dTdx..dTdz
 };
 
-// level-2 viscous fields on planes [H-2, nzl+H+2): gradients (inline d1 in
-// residual precision for Storesome; wk-precision ddx1 rounded to the staged
-// arrays' storage for Default), then divu, sum_i u_i tau_ij, dT_j.
-template <class T, class WC, class PT, bool STAGED>
-__global__ void __launch_bounds__(256) k_level2(Geo g, const PT* __restrict__ prim, T* __restrict__ lev2,
-                                                ResConsts rc_, StageConsts sc, DevDiv* div) {
+// ddx1 staging of the Default strategy, materialised (stencil.cpp:11-28
+// called at physics.cpp:503-517): the 12 gradients du_i/dx_j, dT/dx_j at wk
+// compute, rounded to each staged array's storage, written to HBM
+// (grad [12 field][nzl+2H][ny][nx], carrier PT) on planes [H-2, nzl+H+2) --
+// the planes the level-2 fields need, which is what the reference's halo
+// fill of the staged arrays (physics.cpp:510, 515) provides.
+template <class WC, class PT>
+__global__ void __launch_bounds__(256) k_grad(Geo g, const PT* __restrict__ prim, PT* __restrict__ grad,
+                                              StageConsts sc, DevDiv* div) {
+    if (div->key != ~0ull) return;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int p = blockIdx.z + kHalo - 2;
+    if (x >= g.nx || y >= g.ny) return;
+    const auto aw = make_acc<WC, double, PT>(g, nullptr, prim, nullptr, x, y, p);
+    const WC rw = cvt<WC>(sc.r_stage);
+    const long long fs = (long long)g.planes * g.plane;
+    PT* out = grad + (long long)p * g.plane + (long long)y * g.nx + x;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const WC v = d1<WC>([&](int s) { return aw.F(i == 3 ? 4 : i, j, s); }, rw);
+            const int f = i * 3 + j;  // dudx..dwdz, dTdx..dTdz (kGNames order)
+            out[f * fs] = cvt<PT>(round_kind<WC>(sc.kind[f], v));
+        }
+}
+
+// level-2 viscous fields on planes [H-2, nzl+H+2): gradients (GM 0: inline
+// d1 in residual precision, Storesome; GM 1: the Default strategy's
+// wk-precision ddx1 rounded to the staged arrays' storage, formed on the
+// fly; GM 2: the same staged gradients read back from HBM (k_grad), then
+// ld-narrowed like the reference's CView), then divu, sum_i u_i tau_ij, dT_j.
+template <class T, class WC, class PT, int GM>
+__global__ void __launch_bounds__(256) k_level2(Geo g, const PT* __restrict__ prim, const PT* __restrict__ grad,
+                                                T* __restrict__ lev2, ResConsts rc_, StageConsts sc, DevDiv* div) {
     if (div->key != ~0ull) return;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -181,15 +213,16 @@ __global__ void __launch_bounds__(256) k_level2(Geo g, const PT* __restrict__ pr
     if (x >= g.nx || y >= g.ny) return;
     const RC<T> c(rc_);
     const auto a = make_acc<T, double, PT>(g, nullptr, prim, nullptr, x, y, p);
+    const long long fs = (long long)g.planes * g.plane;
     T G[9], dT[3], u[3];
-    if (!STAGED) {
+    if constexpr (GM == 0) {
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int j = 0; j < 3; ++j) G[i * 3 + j] = d1<T>([&](int s) { return a.U(i, j, s); }, c.r);
 #pragma unroll
         for (int j = 0; j < 3; ++j) dT[j] = d1<T>([&](int s) { return a.F(4, j, s); }, c.r);
-    } else {
+    } else if constexpr (GM == 1) {
         const auto aw = make_acc<WC, double, PT>(g, nullptr, prim, nullptr, x, y, p);
         const WC rw = cvt<WC>(sc.r_stage);
 #pragma unroll
@@ -204,12 +237,17 @@ __global__ void __launch_bounds__(256) k_level2(Geo g, const PT* __restrict__ pr
             const WC v = d1<WC>([&](int s) { return aw.F(4, j, s); }, rw);
             dT[j] = cvt<T>(round_kind<WC>(sc.kind[9 + j], v));
         }
+    } else {
+        const PT* gp = grad + (long long)p * g.plane + (long long)y * g.nx + x;
+#pragma unroll
+        for (int f = 0; f < 9; ++f) G[f] = cvt<T>(gp[f * fs]);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) dT[j] = cvt<T>(gp[(9 + j) * fs]);
     }
 #pragma unroll
     for (int i = 0; i < 3; ++i) u[i] = a.U(i, 0, 0);
     T divu, gg[3];
     level2_point<T>(c, G, u, divu, gg);
-    const long long fs = (long long)g.planes * g.plane;
     T* out = lev2 + (long long)p * g.plane + (long long)y * g.nx + x;
     out[0] = divu;
     out[fs] = gg[0];

@@ -348,8 +348,11 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1)
                               xs[xp], yy, 0, zc, mb + b);
             }
         };
+        // the TMA issuer: the last producer thread, whose warp has the fewest
+        // phase-A pairs and rim tasks
+        constexpr int TMA_TID = NP - 1;
         if constexpr (TL::TMA) {
-            if (ptid == 0) {
+            if (ptid == TMA_TID) {
                 tma_issue(zs - 4, 0);
                 if (zs - 3 < ze + 4) tma_issue(zs - 3, 1);
             }
@@ -378,7 +381,7 @@ __global__ void __launch_bounds__(NPW * 32 + TL::NT / 2, 1)
             if constexpr (TL::TMA) {
                 // stage plane p+1 into the buffer plane p-1 used, once every
                 // producer has read it
-                if (ptid == 0 && kk >= 1 && p + 1 < ze + 4) {
+                if (ptid == TMA_TID && kk >= 1 && p + 1 < ze + 4) {
                     mbar_wait(mb + 2 + (sb ^ 1), (unsigned)((kk - 1) >> 1) & 1u);
                     tma_issue(p + 1, sb ^ 1);
                 }

@@ -276,7 +276,9 @@ struct Solver {
     void ipc_setup();
     void ipc_pull(cudaStream_t main, cudaStream_t copy);
     void ipc_wait_consumed(cudaStream_t st, unsigned e);
-    int path = 1;  // 1 fused when available, 0 staged
+    // 1 fused when available; 0 staged; 2 staged with the Default strategy's
+    // gradients materialised in HBM (the reference's dataflow)
+    int path = 1;
     bool halo_fresh = false;
     int qbuf = 0;  // fused path: which Q buffer (and, exact mode, Qt buffer) holds the state
     // Exact-divergence mode (off by default): Qt and R double-buffered, R
@@ -311,6 +313,7 @@ struct Solver {
     int nzl() const { return slabs.empty() ? 0 : slabs[0].geo.nzl; }
     bool fused_ok = false;  // fused kernels compiled for this plan and its wk overrides
     bool use_fused() const { return path == 1 && fused_ok; }
+    bool mat_grads() const { return path == 2 && strategy == MPFD_DEFAULT && viscous; }
     void* qcur(const Slab& s) const { return (use_fused() && qbuf) ? s.q2 : s.q; }
     void* qbuf_ptr(const Slab& s, int b) const { return b ? s.q2 : s.q; }
     void* qtcur(const Slab& s) const { return (use_fused() && exact && qbuf) ? s.qt2 : s.qt; }
@@ -370,7 +373,7 @@ Solver::~Solver() {
     }
     for (auto& s : slabs) {
         cudaSetDevice(s.device);
-        for (void* p : {s.q, s.qt, s.r, s.q2, s.qt2, s.r2, s.prim, s.lev2}) cudaFree(p);
+        for (void* p : {s.q, s.qt, s.r, s.q2, s.qt2, s.r2, s.prim, s.lev2, s.grad}) cudaFree(p);
         cudaFree(s.diag);
         cudaFree(s.partials);
         cudaFree(s.gather);
@@ -775,14 +778,24 @@ static void alloc_staged(Solver& S) {
     const size_t bp = byte_width(S.plan.pk);
     const size_t bl = byte_width(S.plan.mode == 0 ? S.plan.rk : 2);
     for (auto& s : S.slabs) {
-        if (s.prim) continue;
         CK(cudaSetDevice(s.device));
         const size_t el = (size_t)s.geo.planes * s.geo.plane;
-        CK(cudaMalloc(&s.prim, 5 * el * bp));
-        CK(cudaMalloc(&s.lev2, 7 * el * bl));
-        CK(cudaMemsetAsync(s.prim, 0, 5 * el * bp, s.stream));
-        CK(cudaMemsetAsync(s.lev2, 0, 7 * el * bl, s.stream));
-        s.bytes += 5 * el * bp + 7 * el * bl;
+        if (!s.prim) {
+            CK(cudaMalloc(&s.prim, 5 * el * bp));
+            CK(cudaMalloc(&s.lev2, 7 * el * bl));
+            CK(cudaMemsetAsync(s.prim, 0, 5 * el * bp, s.stream));
+            CK(cudaMemsetAsync(s.lev2, 0, 7 * el * bl, s.stream));
+            s.bytes += 5 * el * bp + 7 * el * bl;
+        }
+        if (S.mat_grads() && !s.grad) {
+            // the 12 staged gradient arrays of make_solver_fields (physics.cpp:
+            // 463-473) in the primitives' carrier: every staged value is exact
+            // in it (checked by set_path)
+            const size_t gb = 12 * el * S.launch->grad_carrier_bytes();
+            CK(cudaMalloc(&s.grad, gb));
+            CK(cudaMemsetAsync(s.grad, 0, gb, s.stream));
+            s.bytes += gb;
+        }
     }
 }
 
@@ -1253,7 +1266,7 @@ void Solver::residual_enqueue(int iter, int sub) {
         view.q = qcur(s);
         view.r = rcur(s);
         timed(3, s, [&] { launch->prim(view, pc, iter, sub); });
-        if (viscous) timed(3, s, [&] { launch->level2(view, rc, sc, staged); });
+        if (viscous) timed(3, s, [&] { launch->level2(view, rc, sc, mat_grads() ? 2 : (staged ? 1 : 0)); });
         timed(0, s, [&] { launch->resid(view, rc, iter, sub); });
         CK(cudaGetLastError());
     }
@@ -2015,7 +2028,14 @@ int mpfd_b200_set_overlap(mpfd_solver* h, int enable) {
 int mpfd_b200_set_path(mpfd_solver* h, int path) {
     return guard([&] {
         Solver& S = h->s;
+        if (path < 0 || path > 2) throw ConfigError("path: 0 staged, 1 fused, 2 staged with materialised gradients");
         if (path == 1 && !S.fused_ok) throw ConfigError("fused path not available for this precision plan");
+        if (path == 2) {
+            // every staged gradient value must be exact in the carrier
+            const int ck = S.launch->grad_carrier_bytes() == 8 ? 2 : (S.launch->grad_carrier_bytes() == 4 ? 1 : 0);
+            for (int k : S.kinds_grad)
+                if (k > ck) throw ConfigError("materialised gradients: a gradient override is wider than the carrier");
+        }
         if (path != S.path) {
             S.materialize_r();
             // move the state into the primary buffers before switching

@@ -579,7 +579,13 @@ class Solver:
         return v.value
 
     def set_path(self, path: str):
-        _check(self.L.mpfd_b200_set_path(self.h, 1 if path == "fused" else 0))
+        """"fused" (default), "staged" (one kernel per level) or "materialised"
+        (staged, with the Default strategy's 12 gradients stored in HBM at wk
+        storage -- the reference's dataflow and memory footprint)."""
+        codes = {"staged": 0, "fused": 1, "materialised": 2}
+        if path not in codes:
+            raise ConfigError(f"unknown path '{path}' (expected one of {sorted(codes)})")
+        _check(self.L.mpfd_b200_set_path(self.h, codes[path]))
 
     def set_overlap(self, enable: bool):
         """Overlap the z-halo exchange with the interior planes (default on;

@@ -530,3 +530,46 @@ def test_history_64(b200, preset):
     assert same_bits(got, series[:, :4])
     rel = np.abs(got[:, 1:3] - series[:, 1:3]) / np.abs(series[:, 1:3])
     assert rel.max() <= 1e-12
+
+
+@pytest.mark.parametrize("emulation", EMUL)
+@pytest.mark.parametrize("preset", ["DP", "SPDP-wk", "SPDP-res", "HPSP", "HPSP-res", "HP"])
+def test_materialised_default_gradients(b200, preset, emulation):
+    """The reference's Default dataflow: the 12 ddx1-staged gradients
+    (stencil.cpp:11-28 via physics.cpp:503-517) written to HBM at their wk
+    storage, then read back by the level-2 kernel -- every substep's R, Q and
+    Qt bit for bit the reference's, and the 12 arrays show up in the measured
+    device bytes (the paper's memory table)."""
+    n, dt = 16, 0.002
+    kw = dict(preset=preset, emulation=emulation, strategy="default")
+    s = b200_solver(b200, n, path="materialised", **kw)
+    c = checker(n, **kw)
+    s.init_tgv()
+    c.init()
+    before = s.memory()[0]
+    for it in range(2):
+        for sub in range(3):
+            assert s.evaluate() is None
+            assert c.evaluate()[0] == 0
+            assert_state(s, c, (2,), f"{kw} it{it} sub{sub} R")
+            assert s.rk_substep(sub, dt) is None
+            c.rk_substep(sub, dt)
+            s.fill_state_halos()
+            assert_state(s, c, (0, 1), f"{kw} it{it} sub{sub} Q/Qt")
+    planes, plane = n + 8, n * n
+    # (res, wk) storage bytes; every staged gradient is exact at its wk storage
+    res, wk = {"DP": (8, 8), "SPDP-wk": (8, 4), "SPDP-res": (4, 8), "HPSP": (2, 2), "HPSP-res": (2, 4),
+               "HP": (2, 2)}[preset]
+    lev2 = res if emulation == "strict" else 8  # level-2 fields at the residual compute type
+    grown = s.memory()[0] - before
+    # the 12 gradient arrays, primitives (5) and level-2 fields (7) with
+    # ghost planes, and R (interior)
+    assert grown == (12 * wk + 5 * wk + 7 * lev2) * planes * plane + 5 * n * plane * res
+
+
+def test_materialised_rejects_wide_gradient_override(b200):
+    prec = b200.resolve_preset("HPSP")
+    prec.custom_overrides = {"dTdz": b200.B64}
+    s = b200.Solver(b200.GridSpec(16), prec, "default", b200.FlowParams(0.1, 1600.0, 0.72, 1.4, True))
+    with pytest.raises(b200.ConfigError):
+        s.set_path("materialised")
