@@ -220,6 +220,8 @@ def main():
     ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
                     help="halo transport between ranks: ncclSend/Recv, or copy-engine pulls from "
                          "CUDA-IPC-mapped neighbour buffers (host collectives over gloo)")
+    ap.add_argument("--no-issue-ceiling", action="store_true",
+                    help="skip the issue-ceiling microbenchmark (compute roofline denominators)")
     ap.add_argument("--no-memory-table", action="store_true",
                     help="skip the measured per-preset memory table (Default strategy, materialised)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
@@ -248,7 +250,7 @@ def main():
     gloo = dist.new_group(backend="gloo") if use_nccl and args.transport == "ipc" else None
     hbm, peak_src = peaks()
     try:
-        ceil = m.issue_ceiling(local)
+        ceil = {"skipped": True} if args.no_issue_ceiling else m.issue_ceiling(local)
     except Exception as e:  # report, never hide
         ceil = {"error": str(e)}
 

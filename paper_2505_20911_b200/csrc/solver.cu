@@ -336,6 +336,8 @@ struct Solver {
     void upload_planes(Slab& s, int cls, int comp, const double* src, size_t ld_row, size_t ld_plane, int zb,
                        int nz);
     void get_interior(int cls, int comp, double* dst, size_t ld_row, size_t ld_plane, int off);
+    void set_ext(int cls, int comp, const double* ext3);
+    void get_ext_q(int comp, double* ext3);
     void halo_refresh();
     // overlapped exchange (fused path): off for one slab per process with
     // pz == 1 in LOCAL mode (no neighbour) or slabs too thin to split
@@ -894,6 +896,38 @@ __global__ void k_to_double(const S* __restrict__ src, double* __restrict__ dst,
     dst[i] = cvt<double>(src[pl * src_pitch_plane + o]);
 }
 
+// ext^3 carrier (the reference's Field layout, field.hpp:45-51) <-> slab in
+// whole planes: one contiguous copy per chunk of planes; the device picks the
+// interior (upload) or produces the periodic x/y halo columns and rows
+// (download, fill_halos_periodic's x and y passes, field.cpp:9-28)
+template <class S>
+__global__ void k_from_ext(const double* __restrict__ src, S* __restrict__ dst, long long count, int n, int e,
+                           long long dst_pitch_plane) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const long long nn = (long long)n * n;
+    const long long pl = i / nn;
+    const long long r = i - pl * nn;
+    const int y = (int)(r / n), x = (int)(r - (long long)y * n);
+    dst[pl * dst_pitch_plane + r] = cvt<S>(src[pl * e * e + (long long)(y + 4) * e + x + 4]);
+}
+template <class S>
+__global__ void k_to_ext(const S* __restrict__ src, double* __restrict__ dst, long long count, int n, int e,
+                         long long src_pitch_plane) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const long long ee = (long long)e * e;
+    const long long pl = i / ee;
+    const long long r = i - pl * ee;
+    const int jj = (int)(r / e), ii = (int)(r - (long long)jj * e);
+    int x = ii - 4, y = jj - 4;
+    x += x < 0 ? n : 0;
+    x -= x >= n ? n : 0;
+    y += y < 0 ? n : 0;
+    y -= y >= n ? n : 0;
+    dst[i] = cvt<double>(src[pl * src_pitch_plane + (long long)y * n + x]);
+}
+
 template <class F>
 static void with_kind(int k, F&& f) {
     if (k == 0) f(__half{});
@@ -945,6 +979,73 @@ void Solver::set_interior(int cls, int comp, const double* src, size_t ld_row, s
         r_state = R_MAT;
     }
     for (auto& s : slabs) upload_slab(s, cls, comp, src + off + (size_t)s.geo.z0 * ld_plane, ld_row, ld_plane);
+}
+
+// set_state / get_state on the ext^3 carrier: planes [z0 + 4, z0 + nzl + 4)
+// of the carrier for every slab of this process, whole planes per copy, one
+// synchronisation at the end (the stream orders the reuse of the staging
+// buffer).  Download of Q also writes the x/y halos of those planes.
+void Solver::set_ext(int cls, int comp, const double* ext3) {
+    if (cls < 0 || cls > 2 || comp < 0 || comp > 4) throw ConfigError("bad class/component");
+    if (cls == 2) {
+        materialize_r();
+        ensure_r();
+        r_state = R_MAT;
+    }
+    const int kind = cls == 0 ? plan.qk : (cls == 1 ? plan.tk : plan.rk);
+    const long long e = n + 8, ee = e * e;
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        if (cls == 0) ipc_wait_consumed(s.stream, epoch);
+        const long long pl = s.geo.plane;
+        const int planes_per = (int)std::max<long long>(1, (long long)s.staging_elems / ee);
+        void* base = cls == 0 ? qcur(s) : (cls == 1 ? qtcur(s) : rcur(s));
+        for (int z = 0; z < s.geo.nzl; z += planes_per) {
+            const int nzc = std::min(planes_per, s.geo.nzl - z);
+            CK(cudaMemcpyAsync(s.staging, ext3 + (size_t)(s.geo.z0 + z + kHalo) * ee, (size_t)nzc * ee * sizeof(double),
+                               cudaMemcpyHostToDevice, s.stream));
+            const long long count = (long long)nzc * pl;
+            const long long zoff = cls == 0 ? z + kHalo : z;
+            with_kind(kind, [&](auto tag) {
+                using S = decltype(tag);
+                k_from_ext<S><<<(unsigned)((count + 255) / 256), 256, 0, s.stream>>>(
+                    s.staging, (S*)base + (zoff * 5 + comp) * pl, count, n, (int)e, 5 * pl);
+            });
+            CK(cudaGetLastError());
+        }
+    }
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        CK(cudaStreamSynchronize(s.stream));
+    }
+    if (cls == 0) halo_fresh = false;
+}
+
+void Solver::get_ext_q(int comp, double* ext3) {
+    if (comp < 0 || comp > 4) throw ConfigError("bad class/component");
+    const long long e = n + 8, ee = e * e;
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        const long long pl = s.geo.plane;
+        const int planes_per = (int)std::max<long long>(1, (long long)s.staging_elems / ee);
+        const void* base = qcur(s);
+        for (int z = 0; z < s.geo.nzl; z += planes_per) {
+            const int nzc = std::min(planes_per, s.geo.nzl - z);
+            const long long count = (long long)nzc * ee;
+            with_kind(plan.qk, [&](auto tag) {
+                using S = decltype(tag);
+                k_to_ext<S><<<(unsigned)((count + 255) / 256), 256, 0, s.stream>>>(
+                    (const S*)base + ((long long)(z + kHalo) * 5 + comp) * pl, s.staging, count, n, (int)e, 5 * pl);
+            });
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(ext3 + (size_t)(s.geo.z0 + z + kHalo) * ee, s.staging, (size_t)count * sizeof(double),
+                               cudaMemcpyDeviceToHost, s.stream));
+        }
+    }
+    for (auto& s : slabs) {
+        CK(cudaSetDevice(s.device));
+        CK(cudaStreamSynchronize(s.stream));
+    }
 }
 
 void Solver::get_interior(int cls, int comp, double* dst, size_t ld_row, size_t ld_plane, int off) {
@@ -1598,8 +1699,7 @@ int mpfd_b200_init_uniform(mpfd_solver* s) {
 
 int mpfd_b200_set_state(mpfd_solver* s, int cls, int comp, const double* ext3) {
     return guard([&] {
-        const size_t e = (size_t)s->s.n + 8;  // x, y extent; z extent nzg + 8
-        s->s.set_interior(cls, comp, ext3, e, e * e, (int)((4 * e + 4) * e + 4));
+        s->s.set_ext(cls, comp, ext3);  // x, y extent n + 8; z extent nzg + 8
         s->s.reset_div();
         return MPFD_OK;
     });
@@ -1609,29 +1709,17 @@ int mpfd_b200_get_state(mpfd_solver* s, int cls, int comp, double* ext3) {
         const int n = s->s.n;
         const size_t nz = (size_t)s->s.nzg;
         const size_t e = (size_t)n + 8;
-        s->s.get_interior(cls, comp, ext3, e, e * e, (int)((4 * e + 4) * e + 4));
-        // periodic halos (fill_halos_periodic, field.cpp:9-48) for Q; the
-        // reference never fills Qt/R halos, which stay zero
+        // periodic halos (fill_halos_periodic, field.cpp:9-48) for Q: x and y
+        // on the device with the interior (get_ext_q), z here; the reference
+        // never fills Qt/R halos, which stay zero
         if (cls == 0) {
-            for (size_t kk = 4; kk < nz + 4; ++kk)
-                for (size_t jj = 4; jj < (size_t)n + 4; ++jj) {
-                    double* row = ext3 + (kk * e + jj) * e;
-                    for (int hh = 0; hh < 4; ++hh) {
-                        row[hh] = row[hh + n];
-                        row[4 + n + hh] = row[4 + hh];
-                    }
-                }
-            for (size_t kk = 4; kk < nz + 4; ++kk) {
-                double* pl = ext3 + kk * e * e;
-                for (int hh = 0; hh < 4; ++hh) {
-                    std::memcpy(pl + hh * e, pl + (hh + n) * e, e * sizeof(double));
-                    std::memcpy(pl + (4 + n + hh) * e, pl + (4 + hh) * e, e * sizeof(double));
-                }
-            }
+            s->s.get_ext_q(comp, ext3);
             for (int hh = 0; hh < 4; ++hh) {
                 std::memcpy(ext3 + hh * e * e, ext3 + (hh + nz) * e * e, e * e * sizeof(double));
                 std::memcpy(ext3 + (4 + nz + hh) * e * e, ext3 + (4 + hh) * e * e, e * e * sizeof(double));
             }
+        } else {
+            s->s.get_interior(cls, comp, ext3, e, e * e, (int)((4 * e + 4) * e + 4));
         }
         return MPFD_OK;
     });

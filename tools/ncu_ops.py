@@ -28,13 +28,18 @@ def sass_ops(path, preset):
     fh = gzip.open(path, "rt") if path.endswith(".gz") else open(path)
     tot = 0
     n_all = 0
+    seen = set()  # an inlined instruction is listed under every source line it maps to
     for r in csv.reader(fh):
         if len(r) < 9 or r[0] != "":
             continue
         try:
             n = int(r[8] or 0)
+            addr = int(r[2], 16)
         except ValueError:
             continue
+        if addr in seen:
+            continue
+        seen.add(addr)
         src = r[3].strip()
         if not src:
             continue
@@ -51,8 +56,9 @@ def raw_metrics(path):
     rows = list(csv.reader(open(path)))
     h, vals = rows[0], rows[2]
     d = dict(zip(h, vals))
-    st = sorted(((float(d[k]), k[34:-29]) for k in h
-                 if re.match(r"smsp__average_warps_issue_stalled_.*_per_issue_active.ratio", k)), reverse=True)
+    pre, suf = "smsp__average_warps_issue_stalled_", "_per_issue_active.ratio"
+    st = sorted(((float(d[k]), k[len(pre):-len(suf)]) for k in h
+                 if k.startswith(pre) and k.endswith(suf)), reverse=True)
     return d, st
 
 
@@ -73,7 +79,7 @@ def main():
             float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"]), 1)
         out[f"{preset}/fused/warps_active_pct"] = round(
             float(d["sm__warps_active.avg.pct_of_peak_sustained_active"]), 1)
-        out[f"{preset}/fused/top_stalls"] = [[name or "wait", round(v, 2)] for v, name in st[:5]]
+        out[f"{preset}/fused/top_stalls"] = [[name, round(v, 2)] for v, name in st[:5]]
         out[f"{preset}/fused/kernel"] = d.get("Kernel Name", "")[:120]
     out["source"] = "tools/ncu_ops.py over ncu --set full captures (256^3, one launch each); see profiles/README.md"
     with open(out_path, "w") as f:

@@ -23,4 +23,4 @@ for k in keys:
     if k.endswith(".sum") and "inst" in k: per = f"{float(v.replace(',', '')) * 32 / pts:.0f} thread-inst"
     print(f"| {k} | {v} | {u.get(k, '')} | {per} |")
 stalls = [(float(d[h]), h) for h in hdr if re.match(r"smsp__average_warps_issue_stalled_.*_per_issue_active.ratio", h)]
-print("\ntop stall reasons (warps per issue): " + ", ".join(f"{h[34:-29]} {v:.2f}" for v, h in sorted(stalls, reverse=True)[:6]))
+print("\ntop stall reasons (warps per issue): " + ", ".join(f"{h[34:-23]} {v:.2f}" for v, h in sorted(stalls, reverse=True)[:6]))

@@ -58,10 +58,10 @@ for P in ("DP", "SPDP", "HPSP", "SP"):
             else "substep 0: read Q, write Q and Qt")
     lines.append(f"\nDRAM bytes per point per launch (mean of the captured launches): {per_pt:.1f}; "
                  f"compulsory ({what}): {comp:.1f}\n")
-    st = [(float(dict(zip(h, vals[0]))[k]), k[34:-29]) for k in h
+    st = [(float(dict(zip(h, vals[0]))[k]), k[34:-23]) for k in h
           if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")]
     lines.append("top stall reasons (warps per issue, launch 0): " +
-                 ", ".join(f"{n or 'wait'} {x:.2f}" for x, n in sorted(st, reverse=True)[:8]) + "\n")
+                 ", ".join(f"{n} {x:.2f}" for x, n in sorted(st, reverse=True)[:8]) + "\n")
 lf = os.path.join(d, "launches.csv")
 if os.path.exists(lf):
     txt = open(lf).read().splitlines()
