@@ -104,6 +104,12 @@ typedef struct {
     const int* devices; /* LOCAL only; NULL -> all slabs on `device` */
     const void* nccl_id;
     const mpfd_hostcomm* hostcomm; /* IPC only */
+    /* y pencils: a 1 x py x pz process grid (ProcessGrid, config.hpp:33;
+     * 0/1 = z-slabs).  LOCAL only, staged path: the pz*py pencils keep 4 y
+     * ghost rows in HBM, exchanged by pack / peer-copy / unpack kernels
+     * before the z planes (which then carry the y-z corners).  `devices`
+     * lists pz*py devices, pencil (iy, iz) at index iz*py + iy. */
+    int py;
 } mpfd_decomp;
 
 /* DivergenceEvent (physics.hpp:85-91); code 1 "nonpositive or nonfinite

@@ -28,8 +28,22 @@ constexpr int kHalo = 4;
 struct Geo {
     int nx, ny, nzl;  // local interior extents
     int z0;           // global z of local plane 0
-    long long plane;  // nx*ny
+    long long plane;  // nx*ny (Qt, R)
     int planes;       // nzl + 2*kHalo
+    // y pencils (staged path): yg ghost rows per side in the HBM arrays of
+    // Q, primitives, level-2 fields and gradients (0: y periodic by index,
+    // the z-slab layout); qplane = nx*(ny + 2*yg) is their plane size; y0
+    // and nyg place the local rows in the global grid
+    int yg;
+    long long qplane;
+    int y0, nyg;
+    // memory row of local row y shifted by s along y (periodic by index
+    // without ghost rows; y is a memory row already when yg > 0)
+    __host__ __device__ __forceinline__ int yrow(int y, int s) const {
+        if (yg) return y + s;
+        const int t = y + s;
+        return t < 0 ? t + ny : (t >= ny ? t - ny : t);
+    }
 };
 
 // divergence record.  Every entry carries its substep key (iteration * 3 +
@@ -104,8 +118,8 @@ __device__ __forceinline__ GlobalAcc<T, QS, PT> make_acc(const Geo& g, const QS*
     a.q = q;
     a.prim = prim;
     a.lev2 = lev2;
-    a.plane = g.plane;
-    a.fstride = (long long)g.planes * g.plane;
+    a.plane = g.qplane;
+    a.fstride = (long long)g.planes * g.qplane;
     a.nx = g.nx;
     a.x = x;
     a.y = y;
@@ -113,7 +127,7 @@ __device__ __forceinline__ GlobalAcc<T, QS, PT> make_acc(const Geo& g, const QS*
 #pragma unroll
     for (int s = -2; s <= 2; ++s) {
         a.wx[s + 2] = wrapi(x + s, g.nx);
-        a.wy[s + 2] = wrapi(y + s, g.ny);
+        a.wy[s + 2] = g.yrow(y, s);
     }
     return a;
 }
@@ -133,37 +147,43 @@ __global__ void __launch_bounds__(256) k_prim(Geo g, const QS* __restrict__ q, P
     if (div->key != ~0ull) return;
     using O = Op<WC>;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;  // memory row (ghost rows included)
     const int p = blockIdx.z;
-    if (x >= g.nx || y >= g.ny) return;
+    if (x >= g.nx || y >= g.ny + 2 * g.yg) return;
     const long long o = (long long)y * g.nx + x;
-    const QS* qp = q + (long long)p * 5 * g.plane + o;
+    const QS* qp = q + (long long)p * 5 * g.qplane + o;
     const WC rho = cvt<WC>(qp[0]);
-    if (p >= kHalo && p < g.nzl + kHalo) {
+    if (p >= kHalo && p < g.nzl + kHalo && y >= g.yg && y < g.yg + g.ny) {
         const float rf = (float)cvt<double>(rho);
         if (!(rf > 0.0f) || !isfinite(rf)) {
             const unsigned long long gi =
-                ((unsigned long long)(g.z0 + p - kHalo) * g.ny + y) * g.nx + x;
+                ((unsigned long long)(g.z0 + p - kHalo) * g.nyg + (g.y0 + y - g.yg)) * g.nx + x;
             record_div(div, 0, 0, gi, iter, sub);
         }
     }
     const WC half = cvt<WC>(pc.half), gm1 = cvt<WC>(pc.gm1), gM2 = cvt<WC>(pc.gM2);
-    const WC ux = O::div(cvt<WC>(qp[g.plane]), rho);
-    const WC uy = O::div(cvt<WC>(qp[2 * g.plane]), rho);
-    const WC uz = O::div(cvt<WC>(qp[3 * g.plane]), rho);
-    const WC Et = O::div(cvt<WC>(qp[4 * g.plane]), rho);
+    const WC ux = O::div(cvt<WC>(qp[g.qplane]), rho);
+    const WC uy = O::div(cvt<WC>(qp[2 * g.qplane]), rho);
+    const WC uz = O::div(cvt<WC>(qp[3 * g.qplane]), rho);
+    const WC Et = O::div(cvt<WC>(qp[4 * g.qplane]), rho);
     const WC kin = O::mul(half, O::add(O::add(O::mul(ux, ux), O::mul(uy, uy)), O::mul(uz, uz)));
     const WC e = O::sub(Et, kin);
     const WC pr = O::mul(gm1, O::mul(rho, e));
     const WC Tv = O::div(O::mul(gM2, pr), rho);
-    const long long fs = (long long)g.planes * g.plane;
-    PT* out = prim + (long long)p * g.plane + o;
+    const long long fs = (long long)g.planes * g.qplane;
+    PT* out = prim + (long long)p * g.qplane + o;
     out[0] = cvt<PT>(round_kind<WC>(pc.kind[0], ux));
     out[fs] = cvt<PT>(round_kind<WC>(pc.kind[1], uy));
     out[2 * fs] = cvt<PT>(round_kind<WC>(pc.kind[2], uz));
     out[3 * fs] = cvt<PT>(round_kind<WC>(pc.kind[3], pr));
     out[4 * fs] = cvt<PT>(round_kind<WC>(pc.kind[4], Tv));
 }
+
+// rows of the level-2 pass: every row (periodic y) or the interior plus the
+// 2-row rim the residual's y-stencils reach (y pencils); memory row of
+// launch row y
+__device__ __forceinline__ int l2_row(const Geo& g, int y) { return g.yg ? y + g.yg - 2 : y; }
+__host__ __device__ __forceinline__ int l2_rows(const Geo& g) { return g.yg ? g.ny + 4 : g.ny; }
 
 struct StageConsts {
     double r_stage;  // cvt_wk(1/(12h)) for ddx1 staging (stencil.cpp:16)
@@ -183,11 +203,12 @@ __global__ void __launch_bounds__(256) k_grad(Geo g, const PT* __restrict__ prim
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     const int p = blockIdx.z + kHalo - 2;
-    if (x >= g.nx || y >= g.ny) return;
-    const auto aw = make_acc<WC, double, PT>(g, nullptr, prim, nullptr, x, y, p);
+    if (x >= g.nx || y >= l2_rows(g)) return;
+    const int ym = l2_row(g, y);
+    const auto aw = make_acc<WC, double, PT>(g, nullptr, prim, nullptr, x, ym, p);
     const WC rw = cvt<WC>(sc.r_stage);
-    const long long fs = (long long)g.planes * g.plane;
-    PT* out = grad + (long long)p * g.plane + (long long)y * g.nx + x;
+    const long long fs = (long long)g.planes * g.qplane;
+    PT* out = grad + (long long)p * g.qplane + (long long)ym * g.nx + x;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -210,10 +231,11 @@ __global__ void __launch_bounds__(256) k_level2(Geo g, const PT* __restrict__ pr
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     const int p = blockIdx.z + kHalo - 2;
-    if (x >= g.nx || y >= g.ny) return;
+    if (x >= g.nx || y >= l2_rows(g)) return;
+    const int ym = l2_row(g, y);
     const RC<T> c(rc_);
-    const auto a = make_acc<T, double, PT>(g, nullptr, prim, nullptr, x, y, p);
-    const long long fs = (long long)g.planes * g.plane;
+    const auto a = make_acc<T, double, PT>(g, nullptr, prim, nullptr, x, ym, p);
+    const long long fs = (long long)g.planes * g.qplane;
     T G[9], dT[3], u[3];
     if constexpr (GM == 0) {
 #pragma unroll
@@ -223,7 +245,7 @@ __global__ void __launch_bounds__(256) k_level2(Geo g, const PT* __restrict__ pr
 #pragma unroll
         for (int j = 0; j < 3; ++j) dT[j] = d1<T>([&](int s) { return a.F(4, j, s); }, c.r);
     } else if constexpr (GM == 1) {
-        const auto aw = make_acc<WC, double, PT>(g, nullptr, prim, nullptr, x, y, p);
+        const auto aw = make_acc<WC, double, PT>(g, nullptr, prim, nullptr, x, ym, p);
         const WC rw = cvt<WC>(sc.r_stage);
 #pragma unroll
         for (int i = 0; i < 3; ++i)
@@ -238,7 +260,7 @@ __global__ void __launch_bounds__(256) k_level2(Geo g, const PT* __restrict__ pr
             dT[j] = cvt<T>(round_kind<WC>(sc.kind[9 + j], v));
         }
     } else {
-        const PT* gp = grad + (long long)p * g.plane + (long long)y * g.nx + x;
+        const PT* gp = grad + (long long)p * g.qplane + (long long)ym * g.nx + x;
 #pragma unroll
         for (int f = 0; f < 9; ++f) G[f] = cvt<T>(gp[f * fs]);
 #pragma unroll
@@ -248,7 +270,7 @@ __global__ void __launch_bounds__(256) k_level2(Geo g, const PT* __restrict__ pr
     for (int i = 0; i < 3; ++i) u[i] = a.U(i, 0, 0);
     T divu, gg[3];
     level2_point<T>(c, G, u, divu, gg);
-    T* out = lev2 + (long long)p * g.plane + (long long)y * g.nx + x;
+    T* out = lev2 + (long long)p * g.qplane + (long long)ym * g.nx + x;
     out[0] = divu;
     out[fs] = gg[0];
     out[2 * fs] = gg[1];
@@ -270,7 +292,7 @@ __global__ void __launch_bounds__(256) k_resid(Geo g, const QS* __restrict__ q, 
     const int z = blockIdx.z;
     if (x >= g.nx || y >= g.ny) return;
     const RC<T> c(rc_);
-    const auto a = make_acc<T, QS, PT>(g, q, prim, lev2, x, y, z + kHalo);
+    const auto a = make_acc<T, QS, PT>(g, q, prim, lev2, x, y + g.yg, z + kHalo);
     T out[5];
     residual_point<T>(c, a, out);
     const long long o = (long long)y * g.nx + x;
@@ -280,7 +302,7 @@ __global__ void __launch_bounds__(256) k_resid(Geo g, const QS* __restrict__ q, 
         const RS v = cvt<RS>(out[comp]);
         rp[comp * g.plane] = v;
         if (!isfinite(cvt<double>(v))) {
-            const unsigned long long gi = ((unsigned long long)(g.z0 + z) * g.ny + y) * g.nx + x;
+            const unsigned long long gi = ((unsigned long long)(g.z0 + z) * g.nyg + (g.y0 + y)) * g.nx + x;
             record_div(div, 1, comp, gi, iter, sub);
         }
     }
@@ -309,7 +331,7 @@ __global__ void __launch_bounds__(256) k_rk(Geo g, QS* __restrict__ q, TS* __res
 #pragma unroll
     for (int comp = 0; comp < 5; ++comp) {
         const long long ir = ((long long)z * 5 + comp) * g.plane + o;
-        const long long iq = ((long long)(z + kHalo) * 5 + comp) * g.plane + o;
+        const long long iq = ((long long)(z + kHalo) * 5 + comp) * g.qplane + o + (long long)g.yg * g.nx;
         const TC t = Op<TC>::mul(dt_c, cvt<TC>(r[ir]));
         const TC v = kc.skip_a ? t : Op<TC>::add(Op<TC>::mul(a_c, cvt<TC>(qt[ir])), t);
         const TS vs = cvt<TS>(v);
@@ -319,7 +341,7 @@ __global__ void __launch_bounds__(256) k_rk(Geo g, QS* __restrict__ q, TS* __res
         q[iq] = ns;
         if (!isfinite(cvt<double>(ns))) {
             const unsigned long long gi =
-                ((unsigned long long)(g.z0 + z) * g.ny + (o / g.nx)) * g.nx + (o % g.nx);
+                ((unsigned long long)(g.z0 + z) * g.nyg + (g.y0 + o / g.nx)) * g.nx + (o % g.nx);
             record_div(div, 2, comp, gi, iter, sub);
         }
     }
@@ -332,26 +354,26 @@ __global__ void __launch_bounds__(256) k_rk(Geo g, QS* __restrict__ q, TS* __res
 template <class QS>
 __device__ __forceinline__ double diag_point(const Geo& g, const QS* __restrict__ q, int x, int y, int z,
                                              int which, int density, double r) {
-    const long long o = (long long)y * g.nx + x;
+    const long long o = (long long)(y + g.yg) * g.nx + x;
     double val;
     if (which == 0) {
-        const QS* qp = q + (long long)(z + kHalo) * 5 * g.plane + o;
+        const QS* qp = q + (long long)(z + kHalo) * 5 * g.qplane + o;
         const double rho = cvt<double>(qp[0]);
-        const double u = __ddiv_rn(cvt<double>(qp[g.plane]), rho);
-        const double v = __ddiv_rn(cvt<double>(qp[2 * g.plane]), rho);
-        const double w = __ddiv_rn(cvt<double>(qp[3 * g.plane]), rho);
+        const double u = __ddiv_rn(cvt<double>(qp[g.qplane]), rho);
+        const double v = __ddiv_rn(cvt<double>(qp[2 * g.qplane]), rho);
+        const double w = __ddiv_rn(cvt<double>(qp[3 * g.qplane]), rho);
         const double k2 =
             __dmul_rn(0.5, __dadd_rn(__dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v)), __dmul_rn(w, w)));
         val = density ? __dmul_rn(rho, k2) : k2;
     } else {
         // velocity component m at offset s along axis d
         auto vel = [&](int m, int d, int s) {
-            int xx = x, yy = y, pp = z + kHalo;
+            int xx = x, yy = y + g.yg, pp = z + kHalo;
             if (d == 0) xx = wrapi(x + s, g.nx);
-            else if (d == 1) yy = wrapi(y + s, g.ny);
+            else if (d == 1) yy = g.yrow(y + g.yg, s);
             else pp += s;
-            const QS* qp = q + (long long)pp * 5 * g.plane + (long long)yy * g.nx + xx;
-            return __ddiv_rn(cvt<double>(qp[(1 + m) * g.plane]), cvt<double>(qp[0]));
+            const QS* qp = q + (long long)pp * 5 * g.qplane + (long long)yy * g.nx + xx;
+            return __ddiv_rn(cvt<double>(qp[(1 + m) * g.qplane]), cvt<double>(qp[0]));
         };
         auto D1 = [&](int m, int d) {
             return d1v<double>(vel(m, d, -2), vel(m, d, -1), vel(m, d, 1), vel(m, d, 2), r);

@@ -251,6 +251,11 @@ struct Solver {
     int viscous = 1;
     double w[7] = {0};
     int pz = 1, mode = MPFD_DECOMP_LOCAL, rank = 0;
+    int py = 1;  // y pencils (LOCAL, staged path)
+    // LOCAL neighbours of slab i = pencil (i % py, i / py), periodic
+    int znb(int i, int dz) const { return ((i / py + dz + pz) % pz) * py + i % py; }
+    int ynb(int i, int dy) const { return (i / py) * py + (i % py + dy + py) % py; }
+    void y_exchange();
     int kinds_prim[5]{}, kinds_grad[12]{};
     KernelPlan plan{};
     std::unique_ptr<Launcher> launch;
@@ -375,7 +380,7 @@ Solver::~Solver() {
     }
     for (auto& s : slabs) {
         cudaSetDevice(s.device);
-        for (void* p : {s.q, s.qt, s.r, s.q2, s.qt2, s.r2, s.prim, s.lev2, s.grad}) cudaFree(p);
+        for (void* p : {s.q, s.qt, s.r, s.q2, s.qt2, s.r2, s.prim, s.lev2, s.grad, s.yface}) cudaFree(p);
         cudaFree(s.diag);
         cudaFree(s.partials);
         cudaFree(s.gather);
@@ -464,28 +469,42 @@ void Solver::setup(const mpfd_grid* grid, const mpfd_precision* p, int strategy_
                           "storeround)");
 
     // decomposition
-    mpfd_decomp d{1, MPFD_DECOMP_LOCAL, 0, 0, nullptr, nullptr};
+    mpfd_decomp d{1, MPFD_DECOMP_LOCAL, 0, 0, nullptr, nullptr, nullptr, 1};
     if (dc) d = *dc;
     pz = d.pz < 1 ? 1 : d.pz;
     mode = d.mode;
     rank = d.rank;
     if (nzg % pz != 0) throw ConfigError("grid nz is not divisible by the z process count");
     if (nzg / pz < kHalo) throw ConfigError("z slab thinner than the halo depth (4)");
+    py = d.py < 1 ? 1 : d.py;
+    if (py > 1) {
+        // y pencils: 1 x py x pz process grid (ProcessGrid, config.hpp:33),
+        // staged path, all pencils in this process
+        if (mode != MPFD_DECOMP_LOCAL) throw ConfigError("y pencils (py > 1) need the LOCAL transport");
+        if (n % py != 0) throw ConfigError("grid ny is not divisible by the y process count");
+        if (n / py < kHalo) throw ConfigError("y pencil thinner than the halo depth (4)");
+    }
     const int nz_local = nzg / pz;
+    const int ny_local = n / py;
     if (mode < MPFD_DECOMP_LOCAL || mode > MPFD_DECOMP_IPC) throw ConfigError("unknown decomposition mode");
     if (dist() && (rank < 0 || rank >= pz)) throw ConfigError("rank out of range");
-    const int nslab = dist() ? 1 : pz;
+    const int nslab = dist() ? 1 : pz * py;
     slabs.resize(nslab);
     for (int i = 0; i < nslab; ++i) {
         Slab& s = slabs[i];
         s.device = (mode == MPFD_DECOMP_LOCAL && d.devices) ? d.devices[i] : d.device;
-        const int r = dist() ? rank : i;
+        // slab i of a LOCAL grid is pencil (iy, iz) = (i % py, i / py)
+        const int r = dist() ? rank : i / py;
         s.geo.nx = n;
-        s.geo.ny = n;
+        s.geo.ny = ny_local;
         s.geo.nzl = nz_local;
         s.geo.z0 = r * nz_local;
-        s.geo.plane = (long long)n * n;
+        s.geo.plane = (long long)n * ny_local;
         s.geo.planes = nz_local + 2 * kHalo;
+        s.geo.yg = py > 1 ? kHalo : 0;
+        s.geo.qplane = (long long)n * (ny_local + 2 * s.geo.yg);
+        s.geo.y0 = (dist() ? 0 : i % py) * ny_local;
+        s.geo.nyg = n;
     }
     if (mode == MPFD_DECOMP_NCCL) {
         if (!d.nccl_id) throw ConfigError("NCCL decomposition needs nccl_id");
@@ -600,6 +619,7 @@ void Solver::ipc_wait_consumed(cudaStream_t st, unsigned e) {
 }
 
 void Solver::alloc() {
+    if (py > 1) fused_ok = false;  // the fused kernels wrap y by index: pencils run the staged path
     const size_t bq = byte_width(plan.qk), bt = byte_width(plan.tk);
     for (size_t i = 0; i < slabs.size(); ++i) {
         Slab& s = slabs[i];
@@ -610,7 +630,7 @@ void Solver::alloc() {
         CK(cudaEventCreateWithFlags(&s.ev_b, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&s.ev_d, cudaEventDisableTiming));
         const size_t pl = (size_t)s.geo.plane;
-        const size_t qel = (size_t)s.geo.planes * 5 * pl;
+        const size_t qel = (size_t)s.geo.planes * 5 * (size_t)s.geo.qplane;
         const size_t iel = (size_t)s.geo.nzl * 5 * pl;
         auto get = [&](void** p, size_t bytes) {
             CK(cudaMalloc(p, bytes));
@@ -781,7 +801,7 @@ static void alloc_staged(Solver& S) {
     const size_t bl = byte_width(S.plan.mode == 0 ? S.plan.rk : 2);
     for (auto& s : S.slabs) {
         CK(cudaSetDevice(s.device));
-        const size_t el = (size_t)s.geo.planes * s.geo.plane;
+        const size_t el = (size_t)s.geo.planes * s.geo.qplane;
         if (!s.prim) {
             CK(cudaMalloc(&s.prim, 5 * el * bp));
             CK(cudaMalloc(&s.lev2, 7 * el * bl));
@@ -928,6 +948,37 @@ __global__ void k_to_ext(const S* __restrict__ src, double* __restrict__ dst, lo
     dst[i] = cvt<double>(src[pl * src_pitch_plane + (long long)y * n + x]);
 }
 
+// y-pencil halo faces (fill_halos_periodic's y pass, field.cpp:20-28,
+// distributed): rows [row0, row0 + H) of the interior planes, all five
+// components, packed into a contiguous [nzl][5][H][nx] buffer that one
+// peer copy moves, and unpacked into the neighbour's ghost rows
+template <class S>
+__global__ void k_pack_yface(const S* __restrict__ q, S* __restrict__ buf, long long count, int nx, int row0,
+                             long long qplane) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int x = (int)(i % nx);
+    long long t = i / nx;
+    const int r = (int)(t % kHalo);
+    t /= kHalo;
+    const int c = (int)(t % 5);
+    const long long z = t / 5;
+    buf[i] = q[((z + kHalo) * 5 + c) * qplane + (long long)(row0 + r) * nx + x];
+}
+template <class S>
+__global__ void k_unpack_yface(const S* __restrict__ buf, S* __restrict__ q, long long count, int nx, int row0,
+                               long long qplane) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int x = (int)(i % nx);
+    long long t = i / nx;
+    const int r = (int)(t % kHalo);
+    t /= kHalo;
+    const int c = (int)(t % 5);
+    const long long z = t / 5;
+    q[((z + kHalo) * 5 + c) * qplane + (long long)(row0 + r) * nx + x] = buf[i];
+}
+
 template <class F>
 static void with_kind(int k, F&& f) {
     if (k == 0) f(__half{});
@@ -944,22 +995,25 @@ void Solver::upload_planes(Slab& s, int cls, int comp, const double* src, size_t
     const int kind = cls == 0 ? plan.qk : (cls == 1 ? plan.tk : plan.rk);
     CK(cudaSetDevice(s.device));
     if (cls == 0) ipc_wait_consumed(s.stream, epoch);  // neighbours may still pull this buffer
-    const long long pl = s.geo.plane;
+    const long long pl = s.geo.plane;                          // interior points per plane
+    const long long apl = cls == 0 ? s.geo.qplane : s.geo.plane;  // array plane (Q: y ghost rows)
+    const long long yoff = cls == 0 ? (long long)s.geo.yg * n : 0;
     const int planes_per = (int)std::max<size_t>(1, s.staging_elems / pl);
+    src += (size_t)s.geo.y0 * ld_row;  // this slab's first row (y pencils)
     for (int z = zb; z < zb + nz; z += planes_per) {
         const int nzc = std::min(planes_per, zb + nz - z);
         for (int zz = 0; zz < nzc; ++zz)
             CK(cudaMemcpy2DAsync(s.staging + (size_t)zz * pl, (size_t)n * sizeof(double),
                                  src + (size_t)(z + zz) * ld_plane, ld_row * sizeof(double),
-                                 (size_t)n * sizeof(double), n, cudaMemcpyHostToDevice, s.stream));
+                                 (size_t)n * sizeof(double), s.geo.ny, cudaMemcpyHostToDevice, s.stream));
         void* base = cls == 0 ? qcur(s) : (cls == 1 ? qtcur(s) : rcur(s));
         const long long count = (long long)nzc * pl;
         const long long zoff = cls == 0 ? z + kHalo : z;
         with_kind(kind, [&](auto tag) {
             using S = decltype(tag);
-            S* dst = (S*)base + (zoff * 5 + comp) * pl;
+            S* dst = (S*)base + (zoff * 5 + comp) * apl + yoff;
             k_from_double<S><<<(unsigned)((count + 255) / 256), 256, 0, s.stream>>>(s.staging, dst, count,
-                                                                                     5 * pl, pl);
+                                                                                     5 * apl, pl);
         });
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(s.stream));
@@ -1056,14 +1110,16 @@ void Solver::get_interior(int cls, int comp, double* dst, size_t ld_row, size_t 
         // zero_temporaries (tgv.cpp:22-25): R has never been written
         for (auto& s : slabs)
             for (int z = 0; z < s.geo.nzl; ++z)
-                for (int y = 0; y < n; ++y)
-                    std::memset(dst + off + (size_t)(s.geo.z0 + z) * ld_plane + (size_t)y * ld_row, 0,
+                for (int y = 0; y < s.geo.ny; ++y)
+                    std::memset(dst + off + (size_t)(s.geo.z0 + z) * ld_plane + (size_t)(s.geo.y0 + y) * ld_row, 0,
                                 (size_t)n * sizeof(double));
         return;
     }
     for (auto& s : slabs) {
         CK(cudaSetDevice(s.device));
         const long long pl = s.geo.plane;
+        const long long apl = cls == 0 ? s.geo.qplane : s.geo.plane;
+        const long long yoff = cls == 0 ? (long long)s.geo.yg * n : 0;
         const int planes_per = (int)std::max<size_t>(1, s.staging_elems / pl);
         for (int z = 0; z < s.geo.nzl; z += planes_per) {
             const int nzc = std::min(planes_per, s.geo.nzl - z);
@@ -1071,17 +1127,17 @@ void Solver::get_interior(int cls, int comp, double* dst, size_t ld_row, size_t 
             const long long count = (long long)nzc * pl;
             with_kind(kind, [&](auto tag) {
                 using S = decltype(tag);
-                const S* srcp = cls == 0 ? (const S*)base + ((long long)(z + kHalo) * 5 + comp) * pl
-                                         : (const S*)base + ((long long)z * 5 + comp) * pl;
+                const S* srcp = cls == 0 ? (const S*)base + ((long long)(z + kHalo) * 5 + comp) * apl + yoff
+                                         : (const S*)base + ((long long)z * 5 + comp) * apl;
                 k_to_double<S><<<(unsigned)((count + 255) / 256), 256, 0, s.stream>>>(srcp, s.staging,
-                                                                                       count, 5 * pl, pl);
+                                                                                       count, 5 * apl, pl);
             });
             CK(cudaGetLastError());
             for (int zz = 0; zz < nzc; ++zz) {
                 const size_t kg = (size_t)(s.geo.z0 + z + zz);
-                CK(cudaMemcpy2DAsync(dst + off + kg * ld_plane, ld_row * sizeof(double),
+                CK(cudaMemcpy2DAsync(dst + off + kg * ld_plane + (size_t)s.geo.y0 * ld_row, ld_row * sizeof(double),
                                      s.staging + (size_t)zz * pl, (size_t)n * sizeof(double),
-                                     (size_t)n * sizeof(double), n, cudaMemcpyDeviceToHost, s.stream));
+                                     (size_t)n * sizeof(double), s.geo.ny, cudaMemcpyDeviceToHost, s.stream));
             }
         }
         CK(cudaStreamSynchronize(s.stream));
@@ -1217,6 +1273,9 @@ void Solver::halo_refresh() {
         halo_fresh = true;
         return;
     }
+    // y pencils: the y faces first (interior planes), so the z pass below
+    // carries the y ghost rows -- and with them the y-z corners
+    if (py > 1) y_exchange();
     // make every slab's interior visible before cross-slab copies
     std::vector<cudaEvent_t> ready(ns);
     for (int i = 0; i < ns; ++i) {
@@ -1226,21 +1285,20 @@ void Solver::halo_refresh() {
     }
     for (int i = 0; i < ns; ++i) {
         Slab& s = slabs[i];
-        const Slab& prv = slabs[(i + ns - 1) % ns];
-        const Slab& nxt = slabs[(i + 1) % ns];
+        const int ip = znb(i, -1), in = znb(i, 1);
+        const Slab& prv = slabs[ip];
+        const Slab& nxt = slabs[in];
         CK(cudaSetDevice(s.device));
-        if (ns > 1) {
-            CK(cudaStreamWaitEvent(s.stream, ready[(i + ns - 1) % ns], 0));
-            CK(cudaStreamWaitEvent(s.stream, ready[(i + 1) % ns], 0));
-        }
-        const size_t blk = (size_t)kHalo * 5 * s.geo.plane * bq;
+        CK(cudaStreamWaitEvent(s.stream, ready[ip], 0));
+        CK(cudaStreamWaitEvent(s.stream, ready[in], 0));
+        const size_t blk = (size_t)kHalo * 5 * s.geo.qplane * bq;
         char* q = (char*)qcur(s);
         const char* pq = (const char*)qcur(prv);
         const char* nq = (const char*)qcur(nxt);
         timed(2, s, [&] {
-            CK(cudaMemcpyPeerAsync(q, s.device, pq + (size_t)prv.geo.nzl * 5 * prv.geo.plane * bq,
+            CK(cudaMemcpyPeerAsync(q, s.device, pq + (size_t)prv.geo.nzl * 5 * prv.geo.qplane * bq,
                                    prv.device, blk, s.stream));
-            CK(cudaMemcpyPeerAsync(q + (size_t)(s.geo.nzl + kHalo) * 5 * s.geo.plane * bq, s.device,
+            CK(cudaMemcpyPeerAsync(q + (size_t)(s.geo.nzl + kHalo) * 5 * s.geo.qplane * bq, s.device,
                                    nq + blk, nxt.device, blk, s.stream));
         });
     }
@@ -1249,13 +1307,81 @@ void Solver::halo_refresh() {
         CK(cudaSetDevice(slabs[i].device));
         CK(cudaEventRecord(ready[i], slabs[i].stream));
     }
-    for (int i = 0; i < ns && ns > 1; ++i) {
+    for (int i = 0; i < ns; ++i) {
         CK(cudaSetDevice(slabs[i].device));
-        CK(cudaStreamWaitEvent(slabs[i].stream, ready[(i + ns - 1) % ns], 0));
-        CK(cudaStreamWaitEvent(slabs[i].stream, ready[(i + 1) % ns], 0));
+        for (int j : {znb(i, -1), znb(i, 1), ynb(i, -1), ynb(i, 1)})
+            if (j != i) CK(cudaStreamWaitEvent(slabs[i].stream, ready[j], 0));
     }
     for (int i = 0; i < ns; ++i) cudaEventDestroy(ready[i]);
     halo_fresh = true;
+}
+
+// y faces of every pencil: pack the 4 boundary rows of each interior plane
+// on the owner, one peer copy per face, unpack into the neighbour's ghost
+// rows (the rows [0, H) take the lower neighbour's top rows, [ny+H, ny+2H)
+// the upper neighbour's bottom rows)
+void Solver::y_exchange() {
+    const size_t bq = byte_width(plan.qk);
+    const int ns = (int)slabs.size();
+    std::vector<cudaEvent_t> packed(ns);
+    for (int i = 0; i < ns; ++i) {
+        Slab& s = slabs[i];
+        CK(cudaSetDevice(s.device));
+        const long long cnt = (long long)s.geo.nzl * 5 * kHalo * s.geo.nx;
+        if (!s.yface) {
+            CK(cudaMalloc(&s.yface, 4 * cnt * bq));  // send lo, send hi, recv lo, recv hi
+            s.bytes += 4 * cnt * bq;
+        }
+        const char* q = (const char*)qcur(s);
+        with_kind(plan.qk, [&](auto tag) {
+            using S = decltype(tag);
+            const unsigned blocks = (unsigned)((cnt + 255) / 256);
+            // bottom interior rows [H, 2H) -> send lo; top rows [ny, ny+H) -> send hi
+            k_pack_yface<S><<<blocks, 256, 0, s.stream>>>((const S*)q, (S*)s.yface, cnt, s.geo.nx, kHalo,
+                                                          s.geo.qplane);
+            k_pack_yface<S><<<blocks, 256, 0, s.stream>>>((const S*)q, (S*)s.yface + cnt, cnt, s.geo.nx, s.geo.ny,
+                                                          s.geo.qplane);
+        });
+        CK(cudaGetLastError());
+        CK(cudaEventCreateWithFlags(&packed[i], cudaEventDisableTiming));
+        CK(cudaEventRecord(packed[i], s.stream));
+    }
+    for (int i = 0; i < ns; ++i) {
+        Slab& s = slabs[i];
+        const Slab& lo = slabs[ynb(i, -1)];
+        const Slab& hi = slabs[ynb(i, 1)];
+        CK(cudaSetDevice(s.device));
+        CK(cudaStreamWaitEvent(s.stream, packed[ynb(i, -1)], 0));
+        CK(cudaStreamWaitEvent(s.stream, packed[ynb(i, 1)], 0));
+        const long long cnt = (long long)s.geo.nzl * 5 * kHalo * s.geo.nx;
+        char* q = (char*)qcur(s);
+        char* rbuf_ = (char*)s.yface + 2 * cnt * bq;
+        timed(2, s, [&] {
+            CK(cudaMemcpyPeerAsync(rbuf_, s.device, (const char*)lo.yface + cnt * bq, lo.device, cnt * bq, s.stream));
+            CK(cudaMemcpyPeerAsync(rbuf_ + cnt * bq, s.device, hi.yface, hi.device, cnt * bq, s.stream));
+        }, 2);
+        with_kind(plan.qk, [&](auto tag) {
+            using S = decltype(tag);
+            const unsigned blocks = (unsigned)((cnt + 255) / 256);
+            k_unpack_yface<S><<<blocks, 256, 0, s.stream>>>((const S*)rbuf_, (S*)q, cnt, s.geo.nx, 0,
+                                                            s.geo.qplane);
+            k_unpack_yface<S><<<blocks, 256, 0, s.stream>>>((const S*)rbuf_ + cnt, (S*)q, cnt, s.geo.nx,
+                                                            s.geo.ny + kHalo, s.geo.qplane);
+        });
+        CK(cudaGetLastError());
+    }
+    // a send buffer is refilled by the next exchange only after both
+    // neighbours copied out of it
+    for (int i = 0; i < ns; ++i) {
+        CK(cudaSetDevice(slabs[i].device));
+        CK(cudaEventRecord(packed[i], slabs[i].stream));
+    }
+    for (int i = 0; i < ns; ++i) {
+        CK(cudaSetDevice(slabs[i].device));
+        for (int j : {ynb(i, -1), ynb(i, 1)})
+            if (j != i) CK(cudaStreamWaitEvent(slabs[i].stream, packed[j], 0));
+    }
+    for (auto& e : packed) cudaEventDestroy(e);
 }
 
 // The z exchange of the current state's ghost planes, enqueued on each slab's
@@ -1536,7 +1662,8 @@ void Solver::diagnostics(int weighting, double t, int threads, mpfd_diag* out) {
     if (!halo_fresh) halo_refresh();
     const size_t N = (size_t)n * n * nzg;
     const size_t nch_total = N / 4096;
-    bool aligned = ((size_t)nzl() * n * n) % 4096 == 0 && N >= 4096;
+    const size_t pblock = (size_t)slabs[0].geo.plane;  // one pencil's points of one plane
+    bool aligned = ((size_t)nzl() * pblock) % 4096 == 0 && N >= 4096 && (py == 1 || pblock % 4096 == 0);
     if (aligned && threads <= 1 && (nch_total & (nch_total - 1)) != 0) aligned = false;
     const double r = 1.0 / (12.0 * h);
     double sums[2];
@@ -1581,6 +1708,22 @@ void Solver::diagnostics(int weighting, double t, int threads, mpfd_diag* out) {
             parts.resize(o + cnt);
             CK(cudaMemcpyAsync(parts.data() + o, src, cnt * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
             CK(cudaStreamSynchronize(s.stream));
+        }
+        if (py > 1) {
+            // y pencils: every pencil's parts are plane by plane; the global
+            // scan order takes, for each plane, the pencils in y order
+            const size_t blk = aligned ? pblock / 4096 : pblock;  // parts per pencil per plane
+            const size_t per_slab = (size_t)nzl() * blk;
+            std::vector<double> g(parts.size());
+            size_t w = 0;
+            for (int iz = 0; iz < pz; ++iz)
+                for (int z = 0; z < nzl(); ++z)
+                    for (int iy = 0; iy < py; ++iy) {
+                        const size_t from = (size_t)(iz * py + iy) * per_slab + (size_t)z * blk;
+                        std::copy(parts.begin() + from, parts.begin() + from + blk, g.begin() + w);
+                        w += blk;
+                    }
+            parts.swap(g);
         }
         if (mode == MPFD_DECOMP_IPC) {
             // every rank's parts in rank (= global z) order
@@ -1699,7 +1842,13 @@ int mpfd_b200_init_uniform(mpfd_solver* s) {
 
 int mpfd_b200_set_state(mpfd_solver* s, int cls, int comp, const double* ext3) {
     return guard([&] {
-        s->s.set_ext(cls, comp, ext3);  // x, y extent n + 8; z extent nzg + 8
+        // x, y extent n + 8; z extent nzg + 8
+        if (s->s.py == 1) {
+            s->s.set_ext(cls, comp, ext3);
+        } else {  // y pencils: row by row
+            const size_t e = (size_t)s->s.n + 8;
+            s->s.set_interior(cls, comp, ext3, e, e * e, (int)((4 * e + 4) * e + 4));
+        }
         s->s.reset_div();
         return MPFD_OK;
     });
@@ -1713,7 +1862,23 @@ int mpfd_b200_get_state(mpfd_solver* s, int cls, int comp, double* ext3) {
         // on the device with the interior (get_ext_q), z here; the reference
         // never fills Qt/R halos, which stay zero
         if (cls == 0) {
-            s->s.get_ext_q(comp, ext3);
+            if (s->s.py == 1) {
+                s->s.get_ext_q(comp, ext3);
+            } else {  // y pencils: row by row, then the x / y halos on the host
+                s->s.get_interior(cls, comp, ext3, e, e * e, (int)((4 * e + 4) * e + 4));
+                for (size_t kk = 4; kk < nz + 4; ++kk) {
+                    double* pl = ext3 + kk * e * e;
+                    for (size_t jj = 4; jj < (size_t)n + 4; ++jj)
+                        for (int hh = 0; hh < 4; ++hh) {
+                            pl[jj * e + hh] = pl[jj * e + hh + n];
+                            pl[jj * e + 4 + n + hh] = pl[jj * e + 4 + hh];
+                        }
+                    for (int hh = 0; hh < 4; ++hh) {
+                        std::memcpy(pl + hh * e, pl + (hh + n) * e, e * sizeof(double));
+                        std::memcpy(pl + (4 + n + hh) * e, pl + (4 + hh) * e, e * sizeof(double));
+                    }
+                }
+            }
             for (int hh = 0; hh < 4; ++hh) {
                 std::memcpy(ext3 + hh * e * e, ext3 + (hh + nz) * e * e, e * e * sizeof(double));
                 std::memcpy(ext3 + (4 + nz + hh) * e * e, ext3 + (4 + hh) * e * e, e * e * sizeof(double));

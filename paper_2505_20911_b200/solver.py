@@ -76,7 +76,7 @@ class _HostComm(C.Structure):
 class _Decomp(C.Structure):
     _fields_ = [("pz", C.c_int), ("mode", C.c_int), ("rank", C.c_int), ("device", C.c_int),
                 ("devices", C.POINTER(C.c_int)), ("nccl_id", C.c_void_p),
-                ("hostcomm", C.POINTER(_HostComm))]
+                ("hostcomm", C.POINTER(_HostComm)), ("py", C.c_int)]
 
 
 class _Div(C.Structure):
@@ -324,6 +324,7 @@ class Decomposition:
     devices: Optional[List[int]] = None
     nccl_id: Optional[bytes] = None
     allgather: Optional[object] = None
+    py: int = 1  # y pencils (LOCAL, staged path): a 1 x py x pz process grid
 
 
 def gloo_allgather(group=None):
@@ -420,7 +421,7 @@ class Solver:
         dd = _Decomp(d.pz, d.mode, d.rank, d.device,
                      self._devs if d.devices else None,
                      C.cast(self._nid, C.c_void_p) if self._nid else None,
-                     C.pointer(self._hc) if self._hc is not None else None)
+                     C.pointer(self._hc) if self._hc is not None else None, d.py)
         self.h = C.c_void_p()
         _check(L.mpfd_b200_create(C.byref(g), C.byref(p), strategy, C.byref(f), C.byref(s),
                                   C.byref(dd), C.byref(self.h)))

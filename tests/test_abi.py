@@ -95,12 +95,11 @@ def test_halo_plan_arithmetic(b200):
 
 def test_no_cpu_fallback_when_library_missing(tmp_path, monkeypatch):
     """The product path fails loudly without its extension."""
-    import importlib
-
     import paper_2505_20911_b200.solver as sv
 
     monkeypatch.setattr(sv, "library_path", str(tmp_path / "missing.so"))
     monkeypatch.setattr(sv, "_lib", None)
     with pytest.raises(ImportError):
         sv.lib()
-    importlib.reload(sv)
+    # monkeypatch restores the loaded library afterwards (no module reload:
+    # that would leave the ctypes argtypes on classes the callers no longer use)
