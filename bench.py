@@ -239,15 +239,23 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # MPFD_BENCH_DEVICE pins every rank to one device: a functional check of
+    # the multi-rank path on a one-GPU box (IPC transport only; the timing of
+    # ranks sharing a GPU is not a scaling number)
+    local = int(os.environ.get("MPFD_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     torch.cuda.set_device(local)
-    use_nccl = world > 1 or args.nccl
+    use_nccl = world > 1 or args.nccl  # multi-rank (the transport is args.transport)
+    ipc = use_nccl and args.transport == "ipc"
     if use_nccl:
         if "RANK" not in os.environ:  # --nccl without a launcher: a 1-rank group
             os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
                               MASTER_PORT=os.environ.get("MASTER_PORT", "29533"))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    gloo = dist.new_group(backend="gloo") if use_nccl and args.transport == "ipc" else None
+        if ipc:  # host collectives only: the halo moves by copy engines
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    gloo = None  # the IPC transport's host all-gather runs on the default (gloo) group
+    red_dev = "cpu" if ipc else "cuda"
     hbm, peak_src = peaks()
     try:
         ceil = {"skipped": True} if args.no_issue_ceiling else m.issue_ceiling(local)
@@ -292,7 +300,7 @@ def main():
             torch.cuda.synchronize()
         ms_total = ev0.elapsed_time(ev1)
         if use_nccl:
-            t = torch.tensor([ms_total], device="cuda")
+            t = torch.tensor([ms_total], device=red_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_total = float(t.item())
         kms, klaunch = s.profile_read()
@@ -341,7 +349,7 @@ def main():
             "path": "fused" if fused else "staged",
         }
         if with_extras and not args.no_e2e:
-            res["e2e"] = (e2e_run_slab(m, s, n, dt, args.steps, world, rank, zper) if use_nccl
+            res["e2e"] = (e2e_run_slab(m, s, n, dt, args.steps, world, rank, zper, red_dev) if use_nccl
                           else e2e_run(m, s, n, dt, args.steps, world, rank))
         mc = s.memory_census()
         bq_ = PRESET_KINDS[preset][0]
@@ -522,7 +530,7 @@ def traffic_lookup(preset, npts, fused):
         return None
 
 
-def e2e_run_slab(m, s, n, dt, steps, world, rank, zper):
+def e2e_run_slab(m, s, n, dt, steps, world, rank, zper, red_dev="cuda"):
     """e2e under the NCCL decomposition: every rank uploads its own z-slab of
     Q from pinned interior binary64 host carriers (the C-ABI's global-index
     set/get with the carrier pointer offset to the slab), advances `steps`
@@ -552,14 +560,14 @@ def e2e_run_slab(m, s, n, dt, steps, world, rank, zper):
     for c in range(5):
         m.solver._check(s.L.mpfd_b200_get_state_interior(s.h, 0, c, C.cast(ptrs[c], C.POINTER(C.c_double))))
     el = time.perf_counter() - t0
-    t = torch.tensor([el], device="cuda")
+    t = torch.tensor([el], device=red_dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     el = float(t.item())
     pts = n * n * nz_glob
     return {"value": pts * steps / el, "unit": UNIT, "h2d_bytes_per_step": 5 * pts * 8 / steps,
             "d2h_bytes_per_step": (5 * pts * 8 + 2 * 2 * (pts // 4096) * 8) / steps,
             "note": "advance() through the C-ABI on every rank: its Q slab uploaded from pinned "
-                    "interior binary64 host carriers, diagnostics sampled at t=0 and t_end (NCCL), "
+                    "interior binary64 host carriers, diagnostics sampled at t=0 and t_end (gathered), "
                     "the slab read back; max over ranks; bytes whole-job, amortised over the steps",
             "diverged": r.diverged}
 
