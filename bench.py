@@ -220,6 +220,9 @@ def main():
     ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
                     help="halo transport between ranks: ncclSend/Recv, or copy-engine pulls from "
                          "CUDA-IPC-mapped neighbour buffers (host collectives over gloo)")
+    ap.add_argument("--slab-sweep", default="2,4,8",
+                    help="LOCAL z-slab counts timed on one GPU (decomposition overhead); '' to skip")
+    ap.add_argument("--slab-preset", default="HPSP")
     ap.add_argument("--no-issue-ceiling", action="store_true",
                     help="skip the issue-ceiling microbenchmark (compute roofline denominators)")
     ap.add_argument("--no-memory-table", action="store_true",
@@ -262,12 +265,14 @@ def main():
     except Exception as e:  # report, never hide
         ceil = {"error": str(e)}
 
-    def measure(preset, with_extras):
+    def measure(preset, with_extras, local_pz=1):
         n = args.grid
         dt = DT.get(n, 2.5e-4)
         prec = m.resolve_preset(preset, args.emulation)
         decomp = None
-        if use_nccl and args.transport == "ipc":
+        if local_pz > 1:  # LOCAL z-slabs on this device (the decomposition's own cost)
+            decomp = m.Decomposition(pz=local_pz, device=local)
+        elif use_nccl and args.transport == "ipc":
             decomp = m.Decomposition(pz=world, mode=m.IPC, rank=rank, device=local,
                                      allgather=m.gloo_allgather(gloo))
         elif use_nccl:
@@ -384,6 +389,21 @@ def main():
             extra[p]["compute"] = r["roofline"]["compute"]
         except Exception as e:  # report, never hide
             extra[p] = {"error": str(e)}
+    # the decomposition's own cost on one GPU: the same grid cut into P
+    # LOCAL z-slabs (ghost-plane recompute, the interior / boundary launch
+    # split, the overlapped exchange by device copies) -- the per-GPU part of
+    # weak-scaling efficiency, everything but the link
+    sweep = {}
+    if world == 1 and args.slab_sweep:
+        base = None
+        for P in [1] + [int(x) for x in args.slab_sweep.split(",") if x]:
+            try:
+                r = measure(args.slab_preset, False, local_pz=P)
+                base = base or r["ms_per_step"]
+                sweep[str(P)] = {"ms_per_step": r["ms_per_step"], "value": r["value"],
+                                 "efficiency_vs_1_slab": base / r["ms_per_step"]}
+            except Exception as e:  # report, never hide
+                sweep[str(P)] = {"error": str(e)}
 
     if rank == 0:
         line = {
@@ -419,6 +439,10 @@ def main():
         }
         if "e2e" in head:
             line["e2e"] = head["e2e"]
+        if sweep:
+            sweep["note"] = (f"{args.slab_preset} {args.grid}^3 cut into P LOCAL z-slabs on one GPU, overlapped "
+                             "exchange: the decomposition's own cost at P GPUs' slab thickness (no link)")
+            line["slab_sweep"] = sweep
         if not args.no_memory_table and world == 1:
             line["memory_table"] = memory_table(m, args, local)
         if "halo" in head:

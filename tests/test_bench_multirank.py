@@ -28,7 +28,7 @@ def test_bench_two_ranks_ipc(b200):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
            "--steps", "3", "--warmup", "3", "--grid", str(n), "--precision", "HPSP", "--transport", "ipc",
-           "--modes", "", "--no-cpu-baseline", "--no-memory-table", "--no-issue-ceiling"]
+           "--modes", "", "--no-cpu-baseline", "--no-memory-table", "--no-issue-ceiling", "--slab-sweep", ""]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600,
                        env={**os.environ, "MPFD_BENCH_DEVICE": "0"})
     assert r.returncode == 0, r.stderr[-3000:]

@@ -8,7 +8,7 @@ for v in ${VARIANTS:-base}; do
   L=paper_2505_20911_b200/libmpfd_b200_$v.so
   [ "$v" = base ] && L=paper_2505_20911_b200/libmpfd_b200.so
   for P in ${PRESETS:-HPSP}; do
-    MPFD_B200_LIB=$PWD/$L timeout 600 python bench.py --precision $P --steps ${STEPS:-5} --warmup 3 --modes "" --no-e2e --no-cpu-baseline > $OUT/bench_${v}_$P.json 2> $OUT/bench_${v}_$P.err
+    MPFD_B200_LIB=$PWD/$L timeout 600 python bench.py --precision $P --steps ${STEPS:-5} --warmup 3 --modes "" --slab-sweep "" --no-e2e --no-cpu-baseline > $OUT/bench_${v}_$P.json 2> $OUT/bench_${v}_$P.err
     python -c "import json; d=json.load(open('$OUT/bench_${v}_$P.json')); print('$v $P', round(d['ms_per_step'],2))" || tail -3 $OUT/bench_${v}_$P.err
   done
 done
