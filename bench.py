@@ -265,7 +265,7 @@ def main():
     except Exception as e:  # report, never hide
         ceil = {"error": str(e)}
 
-    def measure(preset, with_extras, local_pz=1):
+    def measure(preset, with_extras, local_pz=1, overlap=None, zper_override=None):
         n = args.grid
         dt = DT.get(n, 2.5e-4)
         prec = m.resolve_preset(preset, args.emulation)
@@ -282,12 +282,16 @@ def main():
         else:
             decomp = m.Decomposition(device=local)
         zper = world if args.scaling == "weak" else 1
+        if zper_override:
+            zper = zper_override
         s = m.Solver(m.GridSpec(n, z_periods=zper), prec, args.strategy,
                      m.FlowParams(0.1, 1600.0, 0.72, 1.4, True), args.split, decomp)
         if args.path != "auto":
             s.set_path(args.path)
-        if args.no_overlap:
+        if args.no_overlap or overlap is False:
             s.set_overlap(False)
+        elif overlap is True:
+            s.set_overlap(True)
         s.init_tgv()
         s.run_steps(args.warmup, dt)
         s.synchronize()
@@ -397,13 +401,23 @@ def main():
     if world == 1 and args.slab_sweep:
         base = None
         for P in [1] + [int(x) for x in args.slab_sweep.split(",") if x]:
-            try:
-                r = measure(args.slab_preset, False, local_pz=P)
-                base = base or r["ms_per_step"]
-                sweep[str(P)] = {"ms_per_step": r["ms_per_step"], "value": r["value"],
-                                 "efficiency_vs_1_slab": base / r["ms_per_step"]}
-            except Exception as e:  # report, never hide
-                sweep[str(P)] = {"error": str(e)}
+            for ov in ((True,) if P == 1 else (True, False)):
+                key = str(P) if P == 1 else f"{P}/{'overlap' if ov else 'exchange_first'}"
+                try:
+                    r = measure(args.slab_preset, False, local_pz=P, overlap=ov)
+                    base = base or r["ms_per_step"]
+                    sweep[key] = {"ms_per_step": r["ms_per_step"], "value": r["value"],
+                                  "efficiency_vs_1_slab": base / r["ms_per_step"]}
+                except Exception as e:  # report, never hide
+                    sweep[key] = {"error": str(e)}
+        # weak scaling's slab: a whole n^3 period per slab (z_periods = P)
+        P = max([int(x) for x in args.slab_sweep.split(",") if x] or [1])
+        try:
+            r = measure(args.slab_preset, False, local_pz=P, zper_override=P)
+            sweep[f"{P}/weak"] = {"ms_per_step": r["ms_per_step"], "value": r["value"],
+                                  "efficiency_vs_1_slab": r["value"] / (args.grid ** 3 * 1e3 / base)}
+        except Exception as e:
+            sweep[f"{P}/weak"] = {"error": str(e)}
 
     if rank == 0:
         line = {
@@ -420,7 +434,10 @@ def main():
                        "decomposition": f"z-slabs x{world}" + ((" (IPC copy engines)" if args.transport == "ipc"
                                                                   else " (NCCL)") if use_nccl else ""),
                        "halo_exchange": ("overlapped with interior planes (2 streams)"
-                                         if use_nccl and not args.no_overlap else
+                                         if use_nccl and not args.no_overlap
+                                         and args.grid * (world if args.scaling == "weak" else 1) // world >= 128
+                                         else "before each substep (slabs < 128 planes)" if use_nccl
+                                         and not args.no_overlap else
                                          "before each substep" if use_nccl else
                                          "periodic self-copy (1 slab)"),
                        "l2": "state >> 126 MB L2 (no flush needed)"},
@@ -440,8 +457,11 @@ def main():
         if "e2e" in head:
             line["e2e"] = head["e2e"]
         if sweep:
-            sweep["note"] = (f"{args.slab_preset} {args.grid}^3 cut into P LOCAL z-slabs on one GPU, overlapped "
-                             "exchange: the decomposition's own cost at P GPUs' slab thickness (no link)")
+            sweep["note"] = (f"{args.slab_preset}: the {args.grid}^3 grid cut into P LOCAL z-slabs on one GPU "
+                             "(P/overlap: interior launch overlapped with the exchange, then the boundary "
+                             "planes; P/exchange_first: exchange, then one launch), and P slabs of one "
+                             f"{args.grid}^3 period each (P/weak, z_periods = P): the decomposition's own cost at "
+                             "P GPUs' slab thickness, without the link")
             line["slab_sweep"] = sweep
         if not args.no_memory_table and world == 1:
             line["memory_table"] = memory_table(m, args, local)

@@ -310,10 +310,11 @@ int mpfd_b200_issue_ceiling(int device, double out[3]);
  * as the reference holds them.  Bitwise the same results on every path. */
 int mpfd_b200_set_path(mpfd_solver* s, int path);
 /* Overlap of the z-halo exchange with the interior planes (fused path,
- * pz > 1 or NCCL): 1 (default) splits each substep into the interior
- * launch, which runs while the ghost planes are exchanged on a second
- * stream, and the boundary launches after it; 0 exchanges first.  Results
- * are bitwise identical either way. */
+ * pz > 1, NCCL or IPC): 1 splits each substep into the interior launch,
+ * which runs while the ghost planes are exchanged on a second stream, and
+ * the boundary launches after it; 0 exchanges first; -1 (default) overlaps
+ * when the exchange crosses a link and slabs are >= 128 planes thick.
+ * Results are bitwise identical either way. */
 int mpfd_b200_set_overlap(mpfd_solver* s, int enable);
 
 #ifdef __cplusplus

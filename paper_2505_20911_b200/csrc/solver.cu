@@ -346,9 +346,22 @@ struct Solver {
     void halo_refresh();
     // overlapped exchange (fused path): off for one slab per process with
     // pz == 1 in LOCAL mode (no neighbour) or slabs too thin to split
-    int overlap = 1;
+    // -1 auto (default), 0 exchange first, 1 overlap.  Auto overlaps only
+    // where the exchange crosses a link (ranks, or LOCAL slabs on several
+    // devices) and slabs are at least 128 planes thick: on one device the
+    // copies are cheaper than splitting the substep into interior and
+    // boundary launches, and thin slabs pay the split's pipeline start-up on
+    // every boundary CTA (bench slab_sweep)
+    int overlap = -1;
+    bool multi_device() const {
+        for (const auto& s : slabs)
+            if (s.device != slabs[0].device) return true;
+        return false;
+    }
     bool overlap_ok() const {
-        return overlap && use_fused() && (pz > 1 || dist()) && nzl() >= 3 * kHalo;
+        if (!use_fused() || !(pz > 1 || dist()) || nzl() < 3 * kHalo) return false;
+        if (overlap >= 0) return overlap != 0;
+        return (dist() || multi_device()) && nzl() >= 128;
     }
     void exchange_async();
     void residual_enqueue(int iter, int sub);
@@ -2273,7 +2286,7 @@ int mpfd_b200_halo_plan(int n, int pz, int rank, int bytes_q, long long out[9]) 
 int mpfd_b200_set_overlap(mpfd_solver* h, int enable) {
     return guard([&] {
         h->s.sync();
-        h->s.overlap = enable != 0;
+        h->s.overlap = enable < 0 ? -1 : (enable != 0);
         return MPFD_OK;
     });
 }

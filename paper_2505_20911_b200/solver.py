@@ -588,7 +588,9 @@ class Solver:
             raise ConfigError(f"unknown path '{path}' (expected one of {sorted(codes)})")
         _check(self.L.mpfd_b200_set_path(self.h, codes[path]))
 
-    def set_overlap(self, enable: bool):
-        """Overlap the z-halo exchange with the interior planes (default on;
-        bitwise identical results either way)."""
-        _check(self.L.mpfd_b200_set_overlap(self.h, 1 if enable else 0))
+    def set_overlap(self, enable: Optional[bool]):
+        """Overlap the z-halo exchange with the interior planes: True, False,
+        or None for the default policy (overlap where the exchange crosses a
+        link and slabs are >= 128 planes thick).  Bitwise identical results
+        either way."""
+        _check(self.L.mpfd_b200_set_overlap(self.h, -1 if enable is None else (1 if enable else 0)))

@@ -171,9 +171,11 @@ def test_uniform_state_zero_residual(b200, preset):
 CODES = {"nonpositive or nonfinite density": 1, "nonfinite residual": 2, "nonfinite state": 3}
 
 
-def _divergence_run(b200, preset, exact, pz=1, path=None):
+def _divergence_run(b200, preset, exact, pz=1, path=None, overlap=None):
     kw = dict(preset=preset, split="Divergence", viscous=False, mach=0.4)
     s = b200_solver(b200, 16, decomp=b200.Decomposition(pz=pz) if pz > 1 else None, path=path, **kw)
+    if overlap is not None:
+        s.set_overlap(overlap)
     if exact:
         s.set_exact_divergence(True)
     c = checker(16, **kw)
@@ -218,9 +220,10 @@ def test_divergence_event_slabs(b200, pz):
     into the reference's first event; in exact mode the slabs run in
     lock-step per substep and the whole state at the event is the
     reference's."""
-    s, c, _ = _divergence_run(b200, "DP", exact=True, pz=pz)
+    s, c, _ = _divergence_run(b200, "DP", exact=True, pz=pz, overlap=True)
     assert_state(s, c, (0, 1, 2), f"divergence pz={pz} (exact)")
-    _divergence_run(b200, "DP", exact=False, pz=pz)
+    _divergence_run(b200, "DP", exact=False, pz=pz, overlap=True)
+    _divergence_run(b200, "DP", exact=False, pz=pz)  # default: exchange first on one device
 
 
 def test_divergence_event_staged(b200):
@@ -256,6 +259,7 @@ def test_overlapped_exchange_bitwise(b200, preset, pz):
     n = 48
     one = b200_solver(b200, n, preset)
     ov = b200_solver(b200, n, preset, decomp=b200.Decomposition(pz=pz))
+    ov.set_overlap(True)
     seq = b200_solver(b200, n, preset, decomp=b200.Decomposition(pz=pz))
     seq.set_overlap(False)
     runs = []
