@@ -554,13 +554,41 @@ struct FusedPlan {
     static constexpr int MINB2 = STAGE2 ? 1 : ((sizeof(T) == 2 && sizeof(PT) == 2) ? 2 : 1);
     static constexpr size_t SMEM2 = STAGE2 ? staged_smem<TL2>() : FusedSmem<TL2, T, PT>::total;
 
+#ifndef MPFD_ZR
+#define MPFD_ZR 1
+#endif
+    // z planes per CTA.  A CTA fills its 5-plane window with 8 planes it
+    // does not output, and all CTAs of a launch do equal work, so the launch
+    // takes about ceil(CTAs / resident CTAs) waves of (lz + 8) plane-steps:
+    // pick the split that minimises that (thin slabs want fewer, longer CTAs;
+    // MPFD_ZR 0: the round-1 rule, about 8 waves and at least 16 planes)
     static int z_range(const Geo& g, int nz, int tx, int ty, int minb) {
-        // z planes per CTA: about 8 waves of CTAs over the 148 SMs, but at
-        // least 16 planes so the 8-plane start-up of each CTA stays small
         const long long cols = (long long)((g.nx + tx - 1) / tx) * ((g.ny + ty - 1) / ty);
-        const int nzs = (int)std::max<long long>(1, (148LL * minb * 8 + cols - 1) / cols);
-        int lz = (nz + nzs - 1) / nzs;
-        return std::max(lz, std::min(16, nz));
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+                sms = 148;
+        }
+        if (MPFD_ZR == 0) {
+            const int nzs = (int)std::max<long long>(1, (148LL * minb * 8 + cols - 1) / cols);
+            int lz = (nz + nzs - 1) / nzs;
+            return std::max(lz, std::min(16, nz));
+        }
+        const long long slots = (long long)sms * minb;
+        int best = nz;
+        long long best_cost = -1;
+        for (int nzs = 1; nzs <= std::min(nz, 64); ++nzs) {
+            const int lz = (nz + nzs - 1) / nzs;
+            const long long ctas = cols * ((nz + lz - 1) / lz);
+            const long long cost = ((ctas + slots - 1) / slots) * (lz + 8);
+            if (best_cost < 0 || cost < best_cost) {
+                best_cost = cost;
+                best = lz;
+            }
+        }
+        return best;
     }
 
 #ifndef MPFD_WS
