@@ -85,7 +85,7 @@ struct WsBar {
 
 
 #ifndef MPFD_WS_PREG
-#define MPFD_WS_PREG 64
+#define MPFD_WS_PREG 56
 #endif
 #ifndef MPFD_WS32_PREG
 #define MPFD_WS32_PREG 64
