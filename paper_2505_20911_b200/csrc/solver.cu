@@ -263,8 +263,10 @@ struct Solver {
     void* comm = nullptr;
     // IPC transport (one slab per process): the caller's host all-gather,
     // the neighbours' Q buffers and epoch flags mapped with CUDA IPC, and
-    // this rank's flags: [0] the epoch whose boundary planes are final,
-    // [1] / [2] the last epoch the lower / upper neighbour has pulled
+    // this rank's flags, each written by a neighbour and waited on here:
+    // [0] / [3] the epoch whose boundary planes the lower / upper neighbour
+    // has made final, [1] / [2] the last epoch the lower / upper neighbour
+    // has pulled from this rank
     mpfd_hostcomm hc{};
     struct Peer {
         int rank = -1;
@@ -590,13 +592,16 @@ void Solver::ipc_setup() {
 
 // Ghost planes of the current state by copy-engine pulls from both
 // neighbours (fill_halos_periodic's z pass, field.cpp:29-36, distributed).
-// Epoch protocol, all on the GPU (no host sync, no SM):
-//   main stream:  flags[0] = e after the kernels that wrote this state
-//   copy stream:  wait dn.flags[0] >= e, up.flags[0] >= e; pull dn's top and
-//                 up's bottom H interior planes into the ghosts; tell each
-//                 neighbour it has been read (dn.flags[2] = e, up.flags[1] = e)
+// Epoch protocol, all on the GPU (no host sync, no SM); every wait is on
+// this rank's own flags, every signal a write into a neighbour's:
+//   main stream:  after the kernels that wrote this state, tell both
+//                 neighbours it is final (up.flags[0] = e, dn.flags[3] = e)
+//   copy stream:  wait flags[0] >= e and flags[3] >= e (both neighbours'
+//                 states final); pull dn's top and up's bottom H interior
+//                 planes into the ghosts; tell each neighbour it has been
+//                 read (dn.flags[2] = e, up.flags[1] = e)
 // A producer overwrites a published buffer only after both neighbours have
-// pulled it (ipc_wait_consumed).
+// pulled it (ipc_wait_consumed, on flags[1], flags[2]).
 void Solver::ipc_pull(cudaStream_t main, cudaStream_t copy) {
     Slab& s = slabs[0];
     const MemOps& mo = MemOps::get();
@@ -607,13 +612,14 @@ void Solver::ipc_pull(cudaStream_t main, cudaStream_t copy) {
     char* q = (char*)qcur(s);
     const char* dq = (const char*)(alt ? dn_peer.q2 : dn_peer.q);
     const char* uq = (const char*)(alt ? up_peer.q2 : up_peer.q);
-    mo.write(main, flags + 0, e);
+    mo.write(main, up_peer.flags + 0, e);  // to up: its lower neighbour is final
+    mo.write(main, dn_peer.flags + 3, e);  // to dn: its upper neighbour is final
     if (copy != main) {
         CK(cudaEventRecord(s.ev_b, main));
         CK(cudaStreamWaitEvent(copy, s.ev_b, 0));
     }
-    mo.wait_geq(copy, dn_peer.flags + 0, e);
-    mo.wait_geq(copy, up_peer.flags + 0, e);
+    mo.wait_geq(copy, flags + 0, e);
+    mo.wait_geq(copy, flags + 3, e);
     // the neighbours' plans have the same offsets (equal slabs)
     CK(cudaMemcpyAsync(q + hp.recv_lo, dq + hp.send_up, (size_t)hp.block, cudaMemcpyDeviceToDevice, copy));
     CK(cudaMemcpyAsync(q + hp.recv_hi, uq + hp.send_dn, (size_t)hp.block, cudaMemcpyDeviceToDevice, copy));
