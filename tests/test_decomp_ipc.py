@@ -1,4 +1,4 @@
-"""GPU, two processes on one B200: the solver's own multi-rank code path.
+"""GPU, two or three processes on one B200: the solver's own multi-rank code path.
 
 Each process creates a Solver with one z-slab of a pz = 2 decomposition in
 MPFD_DECOMP_IPC mode: the neighbours' Q buffers are mapped with CUDA IPC,
@@ -27,8 +27,10 @@ import torch.multiprocessing as mp
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 CASES = {
-    # name: (n, preset, path, overlap, steps, diag interval, dt, flow kw)
+    # name: (n, preset, path, overlap, steps, diag interval, dt, flow kw[, ranks])
     "hpsp_fused_overlap": (32, "HPSP", "fused", True, 6, 3, 0.002, {}),
+    # three ranks: distinct lower and upper neighbours (two ranks share one)
+    "spdp_three_ranks": (48, "SPDP", "fused", True, 3, 3, 0.002, {"ranks": 3}),
     "dp_fused_no_overlap": (32, "DP", "fused", False, 4, 2, 0.002, {}),
     "spdp_staged": (24, "SPDP", "staged", True, 3, 3, 0.002, {}),
     "diverge": (16, "DP", "fused", True, 400, 10, 0.2, dict(split="Divergence", viscous=False, mach=0.4)),
@@ -53,6 +55,7 @@ def _worker(rank, world, port, name, out_dir):
     import paper_2505_20911_b200 as m
 
     n, preset, path, overlap, steps, di, dt, kw = CASES[name]
+    kw = {k: v for k, v in kw.items() if k != "ranks"}
     flow = m.FlowParams(kw.get("mach", 0.1), 1600.0, 0.72, 1.4, kw.get("viscous", True))
     dec = m.Decomposition(pz=world, mode=m.IPC, rank=rank, device=0, allgather=m.gloo_allgather())
     s = m.Solver(m.GridSpec(n), m.resolve_preset(preset), "storesome", flow, kw.get("split", "Blaisdell"), dec)
@@ -81,21 +84,23 @@ def _worker(rank, world, port, name, out_dir):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", list(CASES))
-def test_ipc_two_ranks_vs_reference(b200, tmp_path, name):
+def test_ipc_ranks_vs_reference(b200, tmp_path, name):
     import pyoracle as po
 
-    world = 2
+    world = CASES[name][7].get("ranks", 2)
     mp.spawn(_worker, args=(world, _free_port(), name, str(tmp_path)), nprocs=world, join=True)
     parts = [pickle.load(open(tmp_path / f"r{r}.pkl", "rb")) for r in range(world)]
     n, preset, path, overlap, steps, di, dt, kw = CASES[name]
+    kw = {k: v for k, v in kw.items() if k != "ranks"}
     ckw = dict(preset=preset, split=kw.get("split", "Blaisdell"), viscous=kw.get("viscous", True),
                mach=kw.get("mach", 0.1))
     c = po.Reference(n, **ckw) if po.ref_available() else po.Oracle(n, **ckw)
     c.init()
     st, series, ev, iters = c.advance(dt, steps, di, threads=8)
-    # both ranks hold the same collective results
-    assert parts[0]["series"] == parts[1]["series"]
-    assert parts[0]["event"] == parts[1]["event"] and parts[0]["iters"] == parts[1]["iters"]
+    # every rank holds the same collective results
+    for p in parts[1:]:
+        assert parts[0]["series"] == p["series"]
+        assert parts[0]["event"] == p["event"] and parts[0]["iters"] == p["iters"]
     assert parts[0]["iters"] == iters
     got = np.array([[t, k, e, d] for t, k, e, d in parts[0]["series"]], dtype=np.float64)
     want = series[:, [0, 1, 2, 4]]
@@ -115,6 +120,6 @@ def test_ipc_two_ranks_vs_reference(b200, tmp_path, name):
             ref = np.stack([c.field(cls, comp)[z0:z0 + nzl] for comp in range(5)])
             assert np.array_equal(p[key].view(np.uint64), ref.view(np.uint64)), (name, key, z0)
         # every state: two pulls of 4 planes x 5 components in q storage
-        bq = 4 if preset == "HPSP" else 8
+        bq = 4 if preset == "HPSP" else 8  # q storage
         blk = 4 * 5 * n * n * bq
         assert p["halo"] % (2 * blk) == 0 and p["halo"] >= 2 * blk * steps * 3
