@@ -2321,6 +2321,23 @@ int mpfd_b200_set_path(mpfd_solver* h, int path) {
                 }
                 S.qbuf = 0;
             }
+            // Q's second buffer exists for the fused kernels only (neighbouring
+            // CTAs read the old Q); the staged paths update Q in place.  IPC
+            // peers keep it mapped, so it stays there.
+            for (auto& s : S.slabs) {
+                const size_t qb = (size_t)s.geo.planes * 5 * s.geo.qplane * byte_width(S.plan.qk);
+                CK(cudaSetDevice(s.device));
+                if (path != 1 && s.q2 && S.mode != MPFD_DECOMP_IPC) {
+                    CK(cudaStreamSynchronize(s.stream));
+                    CK(cudaFree(s.q2));
+                    s.q2 = nullptr;
+                    s.bytes -= qb;
+                } else if (path == 1 && !s.q2) {
+                    CK(cudaMalloc(&s.q2, qb));
+                    CK(cudaMemsetAsync(s.q2, 0, qb, s.stream));
+                    s.bytes += qb;
+                }
+            }
             S.path = path;
         }
         S.sync();
