@@ -279,6 +279,11 @@ struct Solver {
     unsigned epoch = 0;
     std::vector<void*> ipc_mapped;
     bool dist() const { return mode != MPFD_DECOMP_LOCAL; }  // one slab per process
+    int nranks() const { return dist() ? pz * py : 1; }      // ranks of a distributed grid
+    // IPC y pencils: the y neighbours (their packed y faces and flags)
+    Peer ylo_peer, yhi_peer;
+    void* peer_yface_lo = nullptr;  // ylo's send-hi face, mapped
+    void* peer_yface_hi = nullptr;  // yhi's send-lo face, mapped
     void host_allgather(const void* send, void* recv, size_t bytes);
     void ipc_setup();
     void ipc_pull(cudaStream_t main, cudaStream_t copy);
@@ -385,7 +390,7 @@ Solver::~Solver() {
         // its streams and passes the barrier before any memory is released
         try {
             sync();
-            std::vector<char> b((size_t)pz);
+            std::vector<char> b((size_t)nranks());
             char me = 0;
             host_allgather(&me, b.data(), 1);
         } catch (...) {
@@ -494,22 +499,24 @@ void Solver::setup(const mpfd_grid* grid, const mpfd_precision* p, int strategy_
     py = d.py < 1 ? 1 : d.py;
     if (py > 1) {
         // y pencils: 1 x py x pz process grid (ProcessGrid, config.hpp:33),
-        // staged path, all pencils in this process
-        if (mode != MPFD_DECOMP_LOCAL) throw ConfigError("y pencils (py > 1) need the LOCAL transport");
+        // staged path; all pencils in this process (LOCAL) or one per rank
+        // (IPC, rank = iz * py + iy)
+        if (mode == MPFD_DECOMP_NCCL) throw ConfigError("y pencils (py > 1) need the LOCAL or IPC transport");
         if (n % py != 0) throw ConfigError("grid ny is not divisible by the y process count");
         if (n / py < kHalo) throw ConfigError("y pencil thinner than the halo depth (4)");
     }
     const int nz_local = nzg / pz;
     const int ny_local = n / py;
     if (mode < MPFD_DECOMP_LOCAL || mode > MPFD_DECOMP_IPC) throw ConfigError("unknown decomposition mode");
-    if (dist() && (rank < 0 || rank >= pz)) throw ConfigError("rank out of range");
+    if (dist() && (rank < 0 || rank >= pz * (d.py < 1 ? 1 : d.py))) throw ConfigError("rank out of range");
     const int nslab = dist() ? 1 : pz * py;
     slabs.resize(nslab);
     for (int i = 0; i < nslab; ++i) {
         Slab& s = slabs[i];
         s.device = (mode == MPFD_DECOMP_LOCAL && d.devices) ? d.devices[i] : d.device;
-        // slab i of a LOCAL grid is pencil (iy, iz) = (i % py, i / py)
-        const int r = dist() ? rank : i / py;
+        // slab i of a LOCAL grid, or rank i of a distributed one, is pencil
+        // (iy, iz) = (i % py, i / py)
+        const int r = dist() ? rank / py : i / py;
         s.geo.nx = n;
         s.geo.ny = ny_local;
         s.geo.nzl = nz_local;
@@ -518,7 +525,7 @@ void Solver::setup(const mpfd_grid* grid, const mpfd_precision* p, int strategy_
         s.geo.planes = nz_local + 2 * kHalo;
         s.geo.yg = py > 1 ? kHalo : 0;
         s.geo.qplane = (long long)n * (ny_local + 2 * s.geo.yg);
-        s.geo.y0 = (dist() ? 0 : i % py) * ny_local;
+        s.geo.y0 = (dist() ? rank % py : i % py) * ny_local;
         s.geo.nyg = n;
     }
     if (mode == MPFD_DECOMP_NCCL) {
@@ -541,52 +548,114 @@ void Solver::host_allgather(const void* send, void* recv, size_t bytes) {
     if (hc.allgather(hc.ctx, send, recv, bytes) != 0) throw DeviceError("hostcomm allgather failed");
 }
 
+// y-pencil halo faces (fill_halos_periodic's y pass, field.cpp:20-28,
+// distributed): rows [row0, row0 + H) of the interior planes, all five
+// components, packed into a contiguous [nzl][5][H][nx] buffer that one
+// peer copy moves, and unpacked into the neighbour's ghost rows
+template <class S>
+__global__ void k_pack_yface(const S* __restrict__ q, S* __restrict__ buf, long long count, int nx, int row0,
+                             long long qplane) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int x = (int)(i % nx);
+    long long t = i / nx;
+    const int r = (int)(t % kHalo);
+    t /= kHalo;
+    const int c = (int)(t % 5);
+    const long long z = t / 5;
+    buf[i] = q[((z + kHalo) * 5 + c) * qplane + (long long)(row0 + r) * nx + x];
+}
+template <class S>
+__global__ void k_unpack_yface(const S* __restrict__ buf, S* __restrict__ q, long long count, int nx, int row0,
+                               long long qplane) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int x = (int)(i % nx);
+    long long t = i / nx;
+    const int r = (int)(t % kHalo);
+    t /= kHalo;
+    const int c = (int)(t % 5);
+    const long long z = t / 5;
+    q[((z + kHalo) * 5 + c) * qplane + (long long)(row0 + r) * nx + x] = buf[i];
+}
+
+template <class F>
+static void with_kind(int k, F&& f) {
+    if (k == 0) f(__half{});
+    else if (k == 1) f(float{});
+    else f(double{});
+}
+
 // Map the neighbours' Q buffers and flags into this process (CUDA IPC; on
 // peer devices the mapping enables NVLink peer access).  Every rank
 // publishes {q, q2, flags} handles through the host all-gather.
 void Solver::ipc_setup() {
     Slab& s = slabs[0];
     CK(cudaSetDevice(s.device));
-    CK(cudaMalloc(&flags, 4 * sizeof(unsigned)));
-    CK(cudaMemset(flags, 0, 4 * sizeof(unsigned)));
-    s.bytes += 4 * sizeof(unsigned);
+    CK(cudaMalloc(&flags, 8 * sizeof(unsigned)));
+    CK(cudaMemset(flags, 0, 8 * sizeof(unsigned)));
+    s.bytes += 8 * sizeof(unsigned);
+    if (py > 1) {  // packed y faces: send lo, send hi, recv lo, recv hi
+        const size_t face = (size_t)s.geo.nzl * 5 * kHalo * s.geo.nx * byte_width(plan.qk);
+        CK(cudaMalloc(&s.yface, 4 * face));
+        s.bytes += 4 * face;
+    }
     MemOps::get();
     CK(cudaDeviceSynchronize());
     struct Handles {
-        cudaIpcMemHandle_t q, q2, f;
-        int has_q2;
+        cudaIpcMemHandle_t q, q2, f, yf;
+        int has_q2, has_yf;
     } mine{};
     CK(cudaIpcGetMemHandle(&mine.q, s.q));
     if (s.q2) CK(cudaIpcGetMemHandle(&mine.q2, s.q2));
     mine.has_q2 = s.q2 != nullptr;
     CK(cudaIpcGetMemHandle(&mine.f, flags));
-    std::vector<Handles> all((size_t)pz);
+    if (s.yface) CK(cudaIpcGetMemHandle(&mine.yf, s.yface));
+    mine.has_yf = s.yface != nullptr;
+    std::vector<Handles> all((size_t)nranks());
     host_allgather(&mine, all.data(), sizeof(Handles));
-    const int up = (rank + 1) % pz, dn = (rank + pz - 1) % pz;
-    auto open = [&](int r, Peer& p) {
-        p.rank = r;
-        if (r == rank) {  // pz == 1: this rank is its own neighbour
-            p.q = s.q;
-            p.q2 = s.q2;
-            p.flags = flags;
-            return;
-        }
-        auto map = [&](const cudaIpcMemHandle_t& h) {
-            void* ptr = nullptr;
-            CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
-            ipc_mapped.push_back(ptr);
-            return ptr;
-        };
-        p.q = map(all[r].q);
-        p.q2 = all[r].has_q2 ? map(all[r].q2) : nullptr;
-        p.flags = (unsigned*)map(all[r].f);
+    // every neighbour rank is mapped once (with two ranks per axis, or a
+    // pencil grid of 2 x 2, one rank is several neighbours)
+    struct Mapped {
+        void *q, *q2, *yf;
+        unsigned* f;
     };
-    open(dn, dn_peer);
-    if (up == dn) {
-        up_peer = dn_peer;  // pz == 2: one neighbour on both sides, mapped once
-        up_peer.rank = up;
-    } else {
-        open(up, up_peer);
+    std::vector<Mapped> cache((size_t)nranks(), Mapped{nullptr, nullptr, nullptr, nullptr});
+    std::vector<char> done((size_t)nranks(), 0);
+    auto get = [&](int r) -> Mapped {
+        if (r == rank) return Mapped{s.q, s.q2, s.yface, flags};
+        if (!done[r]) {
+            auto map = [&](const cudaIpcMemHandle_t& h) {
+                void* ptr = nullptr;
+                CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+                ipc_mapped.push_back(ptr);
+                return ptr;
+            };
+            cache[r].q = map(all[r].q);
+            cache[r].q2 = all[r].has_q2 ? map(all[r].q2) : nullptr;
+            cache[r].f = (unsigned*)map(all[r].f);
+            cache[r].yf = all[r].has_yf ? map(all[r].yf) : nullptr;
+            done[r] = 1;
+        }
+        return cache[r];
+    };
+    auto peer = [&](int r, Peer& p) {
+        const Mapped m = get(r);
+        p.rank = r;
+        p.q = m.q;
+        p.q2 = m.q2;
+        p.flags = m.f;
+        return m;
+    };
+    const int iz = rank / py, iy = rank % py;
+    peer(((iz + pz - 1) % pz) * py + iy, dn_peer);
+    peer(((iz + 1) % pz) * py + iy, up_peer);
+    if (py > 1) {
+        const size_t face = (size_t)s.geo.nzl * 5 * kHalo * s.geo.nx * byte_width(plan.qk);
+        const Mapped lo = peer(iz * py + (iy + py - 1) % py, ylo_peer);
+        const Mapped hi = peer(iz * py + (iy + 1) % py, yhi_peer);
+        peer_yface_lo = (char*)lo.yf + face;  // its send-hi: its top interior rows
+        peer_yface_hi = hi.yf;                // its send-lo: its bottom interior rows
     }
 }
 
@@ -606,12 +675,54 @@ void Solver::ipc_pull(cudaStream_t main, cudaStream_t copy) {
     Slab& s = slabs[0];
     const MemOps& mo = MemOps::get();
     const size_t bq = byte_width(plan.qk);
-    const HaloPlan hp = halo_plan(n, nzg, pz, rank, (int)bq);
     const unsigned e = ++epoch;
     const bool alt = use_fused() && qbuf;
     char* q = (char*)qcur(s);
     const char* dq = (const char*)(alt ? dn_peer.q2 : dn_peer.q);
     const char* uq = (const char*)(alt ? up_peer.q2 : up_peer.q);
+    // z blocks of a slab (equal slabs: the neighbours' offsets are the same;
+    // mpfd_b200_halo_plan for z-slabs)
+    const size_t plane5 = (size_t)5 * s.geo.qplane * bq;
+    const size_t blk = kHalo * plane5;
+    const size_t send_up = (size_t)s.geo.nzl * plane5, send_dn = blk;
+    const size_t recv_lo = 0, recv_hi = (size_t)(s.geo.nzl + kHalo) * plane5;
+    if (py > 1) {
+        // y pencils (staged path, one stream): the y faces first, so the z
+        // planes below carry the y ghost rows and the y-z corners.  Words
+        // [4] / [7]: the lower / upper y neighbour packed its faces;
+        // [5] / [6]: the lower / upper y neighbour pulled this rank's.
+        const long long cnt = (long long)s.geo.nzl * 5 * kHalo * s.geo.nx;
+        const size_t face = (size_t)cnt * bq;
+        char* yf = (char*)s.yface;
+        mo.wait_geq(main, flags + 5, e - 1);  // the previous faces were pulled
+        mo.wait_geq(main, flags + 6, e - 1);
+        with_kind(plan.qk, [&](auto tag) {
+            using S = decltype(tag);
+            const unsigned blocks = (unsigned)((cnt + 255) / 256);
+            k_pack_yface<S><<<blocks, 256, 0, main>>>((const S*)q, (S*)yf, cnt, s.geo.nx, kHalo, s.geo.qplane);
+            k_pack_yface<S><<<blocks, 256, 0, main>>>((const S*)q, (S*)(yf + face), cnt, s.geo.nx, s.geo.ny,
+                                                      s.geo.qplane);
+        });
+        CK(cudaGetLastError());
+        mo.write(main, ylo_peer.flags + 7, e);  // to ylo: its upper neighbour's faces are packed
+        mo.write(main, yhi_peer.flags + 4, e);
+        mo.wait_geq(main, flags + 4, e);
+        mo.wait_geq(main, flags + 7, e);
+        CK(cudaMemcpyAsync(yf + 2 * face, peer_yface_lo, face, cudaMemcpyDeviceToDevice, main));
+        CK(cudaMemcpyAsync(yf + 3 * face, peer_yface_hi, face, cudaMemcpyDeviceToDevice, main));
+        mo.write(main, ylo_peer.flags + 6, e);  // pulled ylo's upper face
+        mo.write(main, yhi_peer.flags + 5, e);
+        with_kind(plan.qk, [&](auto tag) {
+            using S = decltype(tag);
+            const unsigned blocks = (unsigned)((cnt + 255) / 256);
+            k_unpack_yface<S><<<blocks, 256, 0, main>>>((const S*)(yf + 2 * face), (S*)q, cnt, s.geo.nx, 0,
+                                                        s.geo.qplane);
+            k_unpack_yface<S><<<blocks, 256, 0, main>>>((const S*)(yf + 3 * face), (S*)q, cnt, s.geo.nx,
+                                                        s.geo.ny + kHalo, s.geo.qplane);
+        });
+        CK(cudaGetLastError());
+        halo_sent += 2 * (unsigned long long)face;
+    }
     mo.write(main, up_peer.flags + 0, e);  // to up: its lower neighbour is final
     mo.write(main, dn_peer.flags + 3, e);  // to dn: its upper neighbour is final
     if (copy != main) {
@@ -620,12 +731,11 @@ void Solver::ipc_pull(cudaStream_t main, cudaStream_t copy) {
     }
     mo.wait_geq(copy, flags + 0, e);
     mo.wait_geq(copy, flags + 3, e);
-    // the neighbours' plans have the same offsets (equal slabs)
-    CK(cudaMemcpyAsync(q + hp.recv_lo, dq + hp.send_up, (size_t)hp.block, cudaMemcpyDeviceToDevice, copy));
-    CK(cudaMemcpyAsync(q + hp.recv_hi, uq + hp.send_dn, (size_t)hp.block, cudaMemcpyDeviceToDevice, copy));
+    CK(cudaMemcpyAsync(q + recv_lo, dq + send_up, blk, cudaMemcpyDeviceToDevice, copy));
+    CK(cudaMemcpyAsync(q + recv_hi, uq + send_dn, blk, cudaMemcpyDeviceToDevice, copy));
     mo.write(copy, dn_peer.flags + 2, e);
     mo.write(copy, up_peer.flags + 1, e);
-    halo_sent += 2 * (unsigned long long)hp.block;
+    halo_sent += 2 * (unsigned long long)blk;
 }
 
 // before this rank overwrites the Q buffer that held epoch e: both
@@ -786,7 +896,7 @@ void Solver::substep_barrier() {
         CK(cudaSetDevice(s.device));
         CK(cudaMemcpyAsync(pinned, &s.div->key, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s.stream));
         CK(cudaStreamSynchronize(s.stream));
-        std::vector<unsigned long long> all((size_t)pz);
+        std::vector<unsigned long long> all((size_t)nranks());
         host_allgather(pinned, all.data(), sizeof(unsigned long long));
         unsigned long long key = ULLONG_MAX;
         for (auto v : all) key = std::min(key, v);
@@ -967,43 +1077,6 @@ __global__ void k_to_ext(const S* __restrict__ src, double* __restrict__ dst, lo
     dst[i] = cvt<double>(src[pl * src_pitch_plane + (long long)y * n + x]);
 }
 
-// y-pencil halo faces (fill_halos_periodic's y pass, field.cpp:20-28,
-// distributed): rows [row0, row0 + H) of the interior planes, all five
-// components, packed into a contiguous [nzl][5][H][nx] buffer that one
-// peer copy moves, and unpacked into the neighbour's ghost rows
-template <class S>
-__global__ void k_pack_yface(const S* __restrict__ q, S* __restrict__ buf, long long count, int nx, int row0,
-                             long long qplane) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= count) return;
-    const int x = (int)(i % nx);
-    long long t = i / nx;
-    const int r = (int)(t % kHalo);
-    t /= kHalo;
-    const int c = (int)(t % 5);
-    const long long z = t / 5;
-    buf[i] = q[((z + kHalo) * 5 + c) * qplane + (long long)(row0 + r) * nx + x];
-}
-template <class S>
-__global__ void k_unpack_yface(const S* __restrict__ buf, S* __restrict__ q, long long count, int nx, int row0,
-                               long long qplane) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= count) return;
-    const int x = (int)(i % nx);
-    long long t = i / nx;
-    const int r = (int)(t % kHalo);
-    t /= kHalo;
-    const int c = (int)(t % 5);
-    const long long z = t / 5;
-    q[((z + kHalo) * 5 + c) * qplane + (long long)(row0 + r) * nx + x] = buf[i];
-}
-
-template <class F>
-static void with_kind(int k, F&& f) {
-    if (k == 0) f(__half{});
-    else if (k == 1) f(float{});
-    else f(double{});
-}
 
 // cls 0 Q, 1 Qt, 2 R.  src indexes this slab's local point (i,j,k) at
 // k*ld_plane + j*ld_row + i (binary64 carriers), for local planes
@@ -1625,7 +1698,7 @@ bool Solver::poll_div(bool block) {
     unsigned long long key = ULLONG_MAX;
     for (size_t i = 0; i < slabs.size(); ++i) key = std::min(key, pinned[i]);
     if (mode == MPFD_DECOMP_IPC && block) {
-        std::vector<unsigned long long> all((size_t)pz);
+        std::vector<unsigned long long> all((size_t)nranks());
         host_allgather(&key, all.data(), sizeof key);
         for (auto v : all) key = std::min(key, v);
     }
@@ -1668,9 +1741,9 @@ bool Solver::resolve_div(mpfd_divergence* ev, double dt) {
         CK(cudaStreamSynchronize(s.stream));
         std::memcpy(tot, pinned, sizeof tot);
     } else if (mode == MPFD_DECOMP_IPC) {
-        std::vector<unsigned long long> all((size_t)pz * 15);
+        std::vector<unsigned long long> all((size_t)nranks() * 15);
         host_allgather(tot, all.data(), sizeof tot);
-        return merge_div(all.data(), pz, n, dt, ev);
+        return merge_div(all.data(), nranks(), n, dt, ev);
     }
     return merge_div(tot, 1, n, dt, ev);
 }
@@ -1728,6 +1801,12 @@ void Solver::diagnostics(int weighting, double t, int threads, mpfd_diag* out) {
             CK(cudaMemcpyAsync(parts.data() + o, src, cnt * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
             CK(cudaStreamSynchronize(s.stream));
         }
+        if (mode == MPFD_DECOMP_IPC) {
+            // every rank's parts in rank order (= z, then y pencil)
+            std::vector<double> all(parts.size() * nranks());
+            host_allgather(parts.data(), all.data(), parts.size() * sizeof(double));
+            parts.swap(all);
+        }
         if (py > 1) {
             // y pencils: every pencil's parts are plane by plane; the global
             // scan order takes, for each plane, the pencils in y order
@@ -1743,12 +1822,6 @@ void Solver::diagnostics(int weighting, double t, int threads, mpfd_diag* out) {
                         w += blk;
                     }
             parts.swap(g);
-        }
-        if (mode == MPFD_DECOMP_IPC) {
-            // every rank's parts in rank (= global z) order
-            std::vector<double> all(parts.size() * pz);
-            host_allgather(parts.data(), all.data(), parts.size() * sizeof(double));
-            parts.swap(all);
         }
         const double sum = merge_diag(parts.data(), parts.size(), N, threads, aligned);
         sums[which] = sum;

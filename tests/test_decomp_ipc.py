@@ -31,6 +31,9 @@ CASES = {
     "hpsp_fused_overlap": (32, "HPSP", "fused", True, 6, 3, 0.002, {}),
     # three ranks: distinct lower and upper neighbours (two ranks share one)
     "spdp_three_ranks": (48, "SPDP", "fused", True, 3, 3, 0.002, {"ranks": 3}),
+    # y pencils (staged path): a 2 x 2 grid of ranks, and 3 pencils in y
+    "dp_pencils_2x2": (32, "DP", "staged", False, 3, 3, 0.002, {"ranks": 4, "py": 2}),
+    "hpsp_pencils_1x3": (24, "HPSP", "staged", False, 3, 3, 0.002, {"ranks": 3, "py": 3}),
     "dp_fused_no_overlap": (32, "DP", "fused", False, 4, 2, 0.002, {}),
     "spdp_staged": (24, "SPDP", "staged", True, 3, 3, 0.002, {}),
     "diverge": (16, "DP", "fused", True, 400, 10, 0.2, dict(split="Divergence", viscous=False, mach=0.4)),
@@ -55,20 +58,23 @@ def _worker(rank, world, port, name, out_dir):
     import paper_2505_20911_b200 as m
 
     n, preset, path, overlap, steps, di, dt, kw = CASES[name]
-    kw = {k: v for k, v in kw.items() if k != "ranks"}
+    py = kw.get("py", 1)
+    kw = {k: v for k, v in kw.items() if k not in ("ranks", "py")}
     flow = m.FlowParams(kw.get("mach", 0.1), 1600.0, 0.72, 1.4, kw.get("viscous", True))
-    dec = m.Decomposition(pz=world, mode=m.IPC, rank=rank, device=0, allgather=m.gloo_allgather())
+    dec = m.Decomposition(pz=world // py, py=py, mode=m.IPC, rank=rank, device=0,
+                          allgather=m.gloo_allgather())
     s = m.Solver(m.GridSpec(n), m.resolve_preset(preset), "storesome", flow, kw.get("split", "Blaisdell"), dec)
     s.set_path(path)
     s.set_overlap(overlap)
     s.init_tgv()
     r = s.advance(m.StepConfig(dt, steps, di))
-    z0 = rank * (n // world)
-    nzl = n // world
+    pz = world // py
+    nzl, nyl = n // pz, n // py
+    z0, y0 = (rank // py) * nzl, (rank % py) * nyl
     res = {
-        "z0": z0,
-        "q": np.stack([s.get_field(0, c)[z0:z0 + nzl] for c in range(5)]),
-        "qt": np.stack([s.get_field(1, c)[z0:z0 + nzl] for c in range(5)]),
+        "z0": z0, "y0": y0,
+        "q": np.stack([s.get_field(0, c)[z0:z0 + nzl, y0:y0 + nyl] for c in range(5)]),
+        "qt": np.stack([s.get_field(1, c)[z0:z0 + nzl, y0:y0 + nyl] for c in range(5)]),
         "series": [(x.t, x.kinetic_energy, x.enstrophy, x.diverged) for x in r.series],
         "diverged": r.diverged,
         "event": None if r.divergence is None else tuple(vars(r.divergence).values()),
@@ -91,7 +97,8 @@ def test_ipc_ranks_vs_reference(b200, tmp_path, name):
     mp.spawn(_worker, args=(world, _free_port(), name, str(tmp_path)), nprocs=world, join=True)
     parts = [pickle.load(open(tmp_path / f"r{r}.pkl", "rb")) for r in range(world)]
     n, preset, path, overlap, steps, di, dt, kw = CASES[name]
-    kw = {k: v for k, v in kw.items() if k != "ranks"}
+    py = kw.get("py", 1)
+    kw = {k: v for k, v in kw.items() if k not in ("ranks", "py")}
     ckw = dict(preset=preset, split=kw.get("split", "Blaisdell"), viscous=kw.get("viscous", True),
                mach=kw.get("mach", 0.1))
     c = po.Reference(n, **ckw) if po.ref_available() else po.Oracle(n, **ckw)
@@ -113,13 +120,17 @@ def test_ipc_ranks_vs_reference(b200, tmp_path, name):
         assert [codes[what], i, j, k, it, sub] == ev
         return
     assert not parts[0]["diverged"] and st == 0
-    nzl = n // world
+    pz = world // py
+    nzl, nyl = n // pz, n // py
     for p in parts:
-        z0 = p["z0"]
+        z0, y0 = p["z0"], p["y0"]
         for cls, key in ((0, "q"), (1, "qt")):
-            ref = np.stack([c.field(cls, comp)[z0:z0 + nzl] for comp in range(5)])
-            assert np.array_equal(p[key].view(np.uint64), ref.view(np.uint64)), (name, key, z0)
-        # every state: two pulls of 4 planes x 5 components in q storage
+            ref = np.stack([c.field(cls, comp)[z0:z0 + nzl, y0:y0 + nyl] for comp in range(5)])
+            assert np.array_equal(p[key].view(np.uint64), ref.view(np.uint64)), (name, key, z0, y0)
+        # every state: two pulls of 4 planes x 5 components in q storage (the
+        # planes carry the 4 y ghost rows per side with pencils), plus two
+        # packed y faces of 4 rows
         bq = 4 if preset == "HPSP" else 8  # q storage
-        blk = 4 * 5 * n * n * bq
-        assert p["halo"] % (2 * blk) == 0 and p["halo"] >= 2 * blk * steps * 3
+        rows = nyl + (8 if py > 1 else 0)
+        per_state = 2 * 4 * 5 * rows * n * bq + (2 * nzl * 5 * 4 * n * bq if py > 1 else 0)
+        assert p["halo"] % per_state == 0 and p["halo"] >= per_state * steps * 3
