@@ -105,10 +105,12 @@ typedef struct {
     const void* nccl_id;
     const mpfd_hostcomm* hostcomm; /* IPC only */
     /* y pencils: a 1 x py x pz process grid (ProcessGrid, config.hpp:33;
-     * 0/1 = z-slabs).  LOCAL only, staged path: the pz*py pencils keep 4 y
-     * ghost rows in HBM, exchanged by pack / peer-copy / unpack kernels
-     * before the z planes (which then carry the y-z corners).  `devices`
-     * lists pz*py devices, pencil (iy, iz) at index iz*py + iy. */
+     * 0/1 = z-slabs), staged path.  The pencils keep 4 y ghost rows in HBM,
+     * exchanged by pack / copy / unpack kernels before the z planes (which
+     * then carry the y-z corners).  LOCAL: all pz*py pencils in this
+     * process, `devices` lists pz*py devices, pencil (iy, iz) at index
+     * iz*py + iy.  IPC: one pencil per rank, rank = iz*py + iy, pz*py ranks.
+     * Not with NCCL. */
     int py;
 } mpfd_decomp;
 
