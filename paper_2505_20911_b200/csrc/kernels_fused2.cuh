@@ -653,7 +653,8 @@ struct FusedPlan {
     // TMA staging needs every box of the R4 box contiguous after wrapping:
     // whole tiles in x, 4-row groups in y (tma.cuh)
     static bool tma_ok(const Geo& g) {
-        return g.nx % TLW::TX == 0 && g.ny % 4 == 0 && ((size_t)g.nx * sizeof(QS)) % 16 == 0;
+        // a 4-column rim box must be >= 16 bytes wide: fp32 / fp64 Q only
+        return sizeof(QS) >= 4 && g.nx % TLW::TX == 0 && g.ny % 4 == 0 && ((size_t)g.nx * sizeof(QS)) % 16 == 0;
     }
 
     template <bool ST, unsigned SPL>

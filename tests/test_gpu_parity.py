@@ -317,6 +317,25 @@ def test_64_cubed_step(b200, preset):
     assert_state(s, c, (0, 1), f"64^3 {preset}")
 
 
+@pytest.mark.parametrize("emulation", EMUL)
+@pytest.mark.parametrize("preset", PRESETS)
+def test_fused_64_every_plan(b200, preset, emulation):
+    """Every precision plan on the kernels a 64-multiple grid selects (the
+    TMA-staged warp-specialised fp16 kernel where Q is fp32, the cp.async
+    one where Q is fp16, the fp32 and fp64 kernels): one RK step against the
+    reference, Q and Qt bit for bit."""
+    n, dt = 64, 0.002
+    kw = dict(preset=preset, emulation=emulation)
+    s = b200_solver(b200, n, path="fused", **kw)
+    c = checker(n, **kw)
+    s.init_tgv()
+    c.init()
+    r = s.advance(b200.StepConfig(dt, 1, 0))
+    st, _, _, _ = c.advance(dt, 1, 0)
+    assert not r.diverged and st == 0
+    assert_state(s, c, (0, 1), f"fused 64^3 {kw}")
+
+
 @pytest.mark.parametrize("strategy", STRATS)
 @pytest.mark.parametrize("emulation", EMUL)
 @pytest.mark.parametrize("preset", PRESETS)
