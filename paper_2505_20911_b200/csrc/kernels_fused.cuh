@@ -459,20 +459,10 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
             }
             // rim points: x-rim needs div u, g_x, dT/dx; y-rim div u, g_y, dT/dy
             constexpr int NXR = 4 * TL::TY, NYR = 4 * TL::TX;
-            for (int k = tid; k < NXR + NYR; k += TL::NT) {
-                int rx, ry, dir;
-                if (k < NXR) {
-                    const int col = k / TL::TY;  // 0..3 -> x = -2,-1,TX,TX+1
-                    ry = k - col * TL::TY;
-                    rx = col < 2 ? col - 2 : TL::TX + col - 2;
-                    dir = 0;
-                } else {
-                    const int kk = k - NXR;
-                    const int row = kk / TL::TX;
-                    rx = kk - row * TL::TX;
-                    ry = row < 2 ? row - 2 : TL::TY + row - 2;
-                    dir = 1;
-                }
+            // dir is a compile-time constant in each instance: a runtime
+            // index into G would put the array in local memory
+            auto rim_task = [&](auto dirc, int rx, int ry) {
+                constexpr int dir = decltype(dirc)::value;
                 const int q4 = (ry + 4) * TL::R4X + rx + 4;
                 const int q2 = (ry + 2) * TL::R2X + rx + 2;
                 T G[9], u[3];
@@ -498,6 +488,17 @@ __global__ void __launch_bounds__(TL::NT, MINB) k_fused(FusedArgs a) {
                 Lb[0 * TL::R2N + q2] = divu;
                 Lb[(1 + dir) * TL::R2N + q2] = acc;
                 Lb[(3 + dir) * TL::R2N + q2] = ring_grad<T, WC, PT, TL, STAGED>(plp, q4, 3, dir, c, rw, a.sc);
+            };
+            for (int k = tid; k < NXR + NYR; k += TL::NT) {
+                if (k < NXR) {
+                    const int col = k / TL::TY;  // 0..3 -> x = -2,-1,TX,TX+1
+                    const int ry = k - col * TL::TY;
+                    rim_task(std::integral_constant<int, 0>{}, col < 2 ? col - 2 : TL::TX + col - 2, ry);
+                } else {
+                    const int kk = k - NXR;
+                    const int row = kk / TL::TX;
+                    rim_task(std::integral_constant<int, 1>{}, kk - row * TL::TX, row < 2 ? row - 2 : TL::TY + row - 2);
+                }
             }
         }
         __syncthreads();

@@ -385,20 +385,10 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
             }
             // rim pairs: x-rim pairs (-2,-1) and (TX,TX+1) per row; y-rim rows
             constexpr int NXR = 2 * TL::TY, NYR = 4 * TXP;
-            for (int k = tid; k < NXR + NYR; k += NT) {
-                int rx, ry, dir;
-                if (k < NXR) {
-                    const int col = k / TL::TY;
-                    ry = k - col * TL::TY;
-                    rx = col == 0 ? -2 : TL::TX;
-                    dir = 0;
-                } else {
-                    const int kk = k - NXR;
-                    const int row = kk / TXP;
-                    rx = 2 * (kk - row * TXP);
-                    ry = row < 2 ? row - 2 : TL::TY + row - 2;
-                    dir = 1;
-                }
+            // dir is a compile-time constant in each instance: a runtime
+            // index into G would put the array in local memory
+            auto rim_task = [&](auto dirc, int rx, int ry) {
+                constexpr int dir = decltype(dirc)::value;
                 const int q4 = (ry + 4) * TL::R4X + rx + 4;
                 const int q2 = (ry + 2) * TL::R2X + rx + 2;
                 T2 G[9], u[3];
@@ -424,6 +414,16 @@ __global__ void __launch_bounds__(TL::NT / 2, MINB) k_fused2(FusedArgs a) {
                 stv<T>(Lb + 0 * TL::R2N + q2, divu);
                 stv<T>(Lb + (1 + dir) * TL::R2N + q2, acc);
                 stv<T>(Lb + (3 + dir) * TL::R2N + q2, ring_grad2<T2, WC2, PT, TL, STAGED>(plp, q4, 3, dir, c, rw, a.sc));
+            };
+            for (int k = tid; k < NXR + NYR; k += NT) {
+                if (k < NXR) {
+                    const int col = k / TL::TY;
+                    rim_task(std::integral_constant<int, 0>{}, col == 0 ? -2 : TL::TX, k - col * TL::TY);
+                } else {
+                    const int kk = k - NXR;
+                    const int row = kk / TXP;
+                    rim_task(std::integral_constant<int, 1>{}, 2 * (kk - row * TXP), row < 2 ? row - 2 : TL::TY + row - 2);
+                }
             }
         }
         __syncthreads();
