@@ -78,6 +78,14 @@ __device__ __forceinline__ T2 ring_grad2(const PT* const pl[5], int q, int f, in
         if (j == 1) return ldv<PT>(pl[2] + f * PF + q + s * TL::R4X);
         return ldx<PT>(pl[2] + f * PF + q, s);
     };
+    if constexpr (MPFD_AX != 0 && IsPair<T2>::value && IsPair<WC2>::value) {
+        if (j == 0) {  // the aligned pairs around this pair (stencil.cuh d1x)
+            const PT* b = pl[2] + f * PF + q;
+            if (!STAGED) return d1x<T2>(cvt<T2>(ldv<PT>(b - 2)), cvt<T2>(ldv<PT>(b)), cvt<T2>(ldv<PT>(b + 2)), c.r);
+            const WC2 v = d1x<WC2>(cvt<WC2>(ldv<PT>(b - 2)), cvt<WC2>(ldv<PT>(b)), cvt<WC2>(ldv<PT>(b + 2)), rw);
+            return cvt<T2>(round_kind_v<WC2>(sc.kind[f == 3 ? 9 : f * 3], v));
+        }
+    }
     if (!STAGED) return d1v<T2>(cvt<T2>(val(-2)), cvt<T2>(val(-1)), cvt<T2>(val(1)), cvt<T2>(val(2)), c.r);
     const WC2 v = d1v<WC2>(cvt<WC2>(val(-2)), cvt<WC2>(val(-1)), cvt<WC2>(val(1)), cvt<WC2>(val(2)), rw);
     return cvt<T2>(round_kind_v<WC2>(sc.kind[f == 3 ? 9 + j : f * 3 + j], v));

@@ -15,6 +15,8 @@
 // reusing them is bitwise identical to the reference's inline nesting.
 #pragma once
 
+#include <type_traits>
+
 #include "arith.cuh"
 
 namespace mpfd_b200 {
@@ -85,6 +87,54 @@ __device__ __forceinline__ T d2v(T vm2, T vm1, T v0, T vp1, T vp2, T r2) {
     return O::mul(O::sub(O::sub(O::mul(O::lit(16.0), s1), s2), O::mul(O::lit(30.0), v0)), r2);
 }
 
+// Two-point vectors along x (pair kernels): the pair B = (x, x+1) has its
+// x-neighbours in the aligned pairs A = (x-2, x-1) and C = (x+2, x+3).  A
+// stencil evaluates its operand once on A, B and C (six points, each used)
+// instead of on four shifted pairs, and only the +-1 sums/differences take
+// one lane from each of two pairs -- two scalar ops, where a shifted pair
+// would first be assembled by register moves (fp32) or PRMT (fp16).  Every
+// lane is the same IEEE op on the same operands as d1v / d2v.
+#ifndef MPFD_AX
+#define MPFD_AX 1
+#endif
+// fp32 pairs only: measured SPDP 24.69 -> 24.35 ms, HPSP 13.49 -> 13.71 ms
+// (for half2 the +-1 lanes cost two scalar HADDs plus a PRMT to repack,
+// no cheaper than one PRMT per shifted operand)
+template <class T>
+struct IsPair : std::false_type {};
+template <>
+struct IsPair<float2> : std::true_type {};
+template <class T2>
+__device__ __forceinline__ T2 xsub1(T2 A, T2 B, T2 C) {  // f(+1) - f(-1)
+    using OS = Op<typename ScalarOf<T2>::type>;
+    return Mk<T2>::of(OS::sub(hi(B), hi(A)), OS::sub(lo(C), lo(B)));
+}
+template <class T2>
+__device__ __forceinline__ T2 xadd1(T2 A, T2 B, T2 C) {  // f(+1) + f(-1)
+    using OS = Op<typename ScalarOf<T2>::type>;
+    return Mk<T2>::of(OS::add(hi(B), hi(A)), OS::add(lo(C), lo(B)));
+}
+template <class T2>
+__device__ __forceinline__ T2 d1x(T2 A, T2 B, T2 C, T2 r) {
+    using O = Op<T2>;
+    const T2 s1 = xsub1(A, B, C);
+    const T2 s2 = O::sub(C, A);
+    return O::mul(O::sub(O::mul(O::lit(8.0), s1), s2), r);
+}
+template <class T2>
+__device__ __forceinline__ T2 d2x(T2 A, T2 B, T2 C, T2 r2) {
+    using O = Op<T2>;
+    const T2 s1 = xadd1(A, B, C);
+    const T2 s2 = O::add(C, A);
+    return O::mul(O::sub(O::sub(O::mul(O::lit(16.0), s1), s2), O::mul(O::lit(30.0), B)), r2);
+}
+// d1 of f; AX: f takes the aligned pair index k in {-1, 0, 1} (A, B, C)
+template <class T, bool AX, class F>
+__device__ __forceinline__ T dd1(F&& f, T r) {
+    if constexpr (AX) return d1x<T>(f(-1), f(0), f(1), r);
+    else return d1<T>(f, r);
+}
+
 // phi_value (physics.cpp:82-87)
 template <class T, class Acc>
 __device__ __forceinline__ T phi_val(const Acc& a, int phi, int d, int s) {
@@ -96,7 +146,7 @@ __device__ __forceinline__ T phi_val(const Acc& a, int phi, int d, int s) {
 
 // C_j(phi) at the center, conv_term_point (physics.cpp:93-155).  SPL != 0
 // fixes the active-term mask at compile time (same terms, same order).
-template <class T, unsigned SPL = 0, class Acc>
+template <class T, unsigned SPL = 0, bool AX = false, class Acc>
 __device__ __forceinline__ T conv_term(const RC<T>& c, const Acc& a, int phi, int j) {
     using O = Op<T>;
     const unsigned nzm = SPL ? SPL : c.nz;
@@ -106,7 +156,7 @@ __device__ __forceinline__ T conv_term(const RC<T>& c, const Acc& a, int phi, in
     const T phi0 = need_phi0 ? phi_val<T>(a, phi, j, 0) : O::one();
     T acc = O::zero();
     if (nzm & 0x01u) {  // alpha d(rho u_j phi)
-        const T t = d1<T>(
+        const T t = dd1<T, AX>(
             [&](int s) {
                 if (phi == 0) return a.Q(1 + j, j, s);
                 if (phi == 4) return O::mul(a.Q(4, j, s), a.U(j, j, s));
@@ -116,7 +166,7 @@ __device__ __forceinline__ T conv_term(const RC<T>& c, const Acc& a, int phi, in
         acc = O::add(acc, O::mul(c.coef[0], t));
     }
     if (nzm & 0x02u) {  // beta_rho rho d(u_j phi)
-        const T t = d1<T>(
+        const T t = dd1<T, AX>(
             [&](int s) {
                 if (phi == 0) return a.U(j, j, s);
                 return O::mul(a.U(j, j, s), phi_val<T>(a, phi, j, s));
@@ -125,24 +175,24 @@ __device__ __forceinline__ T conv_term(const RC<T>& c, const Acc& a, int phi, in
         acc = O::add(acc, O::mul(c.coef[1], O::mul(rho0, t)));
     }
     if (nzm & 0x04u) {  // beta_u u_j d(rho phi)
-        const T t = d1<T>([&](int s) { return a.Q(phi, j, s); }, c.r);
+        const T t = dd1<T, AX>([&](int s) { return a.Q(phi, j, s); }, c.r);
         acc = O::add(acc, O::mul(c.coef[2], O::mul(uj0, t)));
     }
     if (nzm & 0x08u) {  // beta_phi phi d(rho u_j)
-        const T t = d1<T>([&](int s) { return a.Q(1 + j, j, s); }, c.r);
+        const T t = dd1<T, AX>([&](int s) { return a.Q(1 + j, j, s); }, c.r);
         acc = O::add(acc, O::mul(c.coef[3], phi == 0 ? t : O::mul(phi0, t)));
     }
     if (nzm & 0x10u) {  // gamma_rho u_j phi d(rho)
-        const T t = d1<T>([&](int s) { return a.Q(0, j, s); }, c.r);
+        const T t = dd1<T, AX>([&](int s) { return a.Q(0, j, s); }, c.r);
         const T uphi = phi == 0 ? uj0 : O::mul(uj0, phi0);
         acc = O::add(acc, O::mul(c.coef[4], O::mul(uphi, t)));
     }
     if (nzm & 0x20u) {  // gamma_u rho phi d(u_j)
-        const T t = d1<T>([&](int s) { return a.U(j, j, s); }, c.r);
+        const T t = dd1<T, AX>([&](int s) { return a.U(j, j, s); }, c.r);
         acc = O::add(acc, O::mul(c.coef[5], O::mul(a.Q(phi, j, 0), t)));
     }
     if ((nzm & 0x40u) && phi != 0) {  // gamma_phi rho u_j d(phi)
-        const T t = d1<T>([&](int s) { return phi_val<T>(a, phi, j, s); }, c.r);
+        const T t = dd1<T, AX>([&](int s) { return phi_val<T>(a, phi, j, s); }, c.r);
         acc = O::add(acc, O::mul(c.coef[6], O::mul(a.Q(1 + j, j, 0), t)));
     }
     return acc;
@@ -264,29 +314,81 @@ template <class T, unsigned SPL = 0, class Acc>
 __device__ __forceinline__ void residual_early_dirwise(const RC<T>& c, const Acc& a, T out[3], Deferred<T>& df) {
     using O = Op<T>;
     T C[5][3], dp[3], pwj[3], lap[3][3], cross[2], tauj[2], hj[2];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        // optional compiler fence between axes (bounds register use; measured:
-        // the unfenced schedule is 6% faster in DP, neutral elsewhere)
+    // the pair kernels' fp32 instance takes the aligned-x form (d1x / d2x);
+    // every other instance keeps this loop as it was (its schedule moves by a
+    // few % with any change to it)
 #ifndef MPFD_AXIS_FENCE
 #define MPFD_AXIS_FENCE 0
 #endif
-        if (MPFD_AXIS_FENCE) asm volatile("" ::: "memory");
-        DirVals<T> v;
-        load_dir<T>(a, j, v);
+    if constexpr (MPFD_AX != 0 && IsPair<T>::value) {
+        auto axis = [&](auto jc) {
+            constexpr int j = decltype(jc)::value;
+            // aligned-x evaluation (d1x / d2x) for the pair kernels' x axis
+            constexpr bool AX = MPFD_AX != 0 && IsPair<T>::value && j == 0;
+            if (MPFD_AXIS_FENCE) asm volatile("" ::: "memory");
+            DirVals<T> v;
+            if constexpr (AX) {
+                // v[k + 2] = the aligned pair at x-offset 2k, k = -1, 0, 1
 #pragma unroll
-        for (int phi = 0; phi < 5; ++phi) C[phi][j] = conv_term<T, SPL>(c, v, phi, j);
-        dp[j] = d1v<T>(v.p[0], v.p[1], v.p[3], v.p[4], c.r);
-        pwj[j] = d1v<T>(O::mul(v.p[0], v.u[j][0]), O::mul(v.p[1], v.u[j][1]), O::mul(v.p[3], v.u[j][3]),
-                        O::mul(v.p[4], v.u[j][4]), c.r);
-        if (c.viscous) {
+                for (int k = -1; k <= 1; ++k) {
 #pragma unroll
-            for (int i = 0; i < 3; ++i)
-                lap[i][j] = d2v<T>(v.u[i][0], v.u[i][1], v.u[i][2], v.u[i][3], v.u[i][4], c.r2);
-            if (j < 2) {
-                cross[j] = d1<T>([&](int s) { return a.DIVU(j, s); }, c.r);
-                tauj[j] = d1<T>([&](int s) { return a.G(j, j, s); }, c.r);
-                hj[j] = d1<T>([&](int s) { return a.DT(j, j, s); }, c.r);
+                    for (int cc = 0; cc < 5; ++cc) v.q[cc][k + 2] = a.Q(cc, 0, 2 * k);
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) v.u[m][k + 2] = a.U(m, 0, 2 * k);
+                    v.p[k + 2] = a.P(0, 2 * k);
+                }
+            } else {
+                load_dir<T>(a, j, v);
+            }
+#pragma unroll
+            for (int phi = 0; phi < 5; ++phi) C[phi][j] = conv_term<T, SPL, AX>(c, v, phi, j);
+            if constexpr (AX) {
+                dp[j] = d1x<T>(v.p[1], v.p[2], v.p[3], c.r);
+                pwj[j] = d1x<T>(O::mul(v.p[1], v.u[j][1]), O::mul(v.p[2], v.u[j][2]), O::mul(v.p[3], v.u[j][3]), c.r);
+            } else {
+                dp[j] = d1v<T>(v.p[0], v.p[1], v.p[3], v.p[4], c.r);
+                pwj[j] = d1v<T>(O::mul(v.p[0], v.u[j][0]), O::mul(v.p[1], v.u[j][1]), O::mul(v.p[3], v.u[j][3]),
+                                O::mul(v.p[4], v.u[j][4]), c.r);
+            }
+            if (c.viscous) {
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    if constexpr (AX) lap[i][j] = d2x<T>(v.u[i][1], v.u[i][2], v.u[i][3], c.r2);
+                    else lap[i][j] = d2v<T>(v.u[i][0], v.u[i][1], v.u[i][2], v.u[i][3], v.u[i][4], c.r2);
+                }
+                if constexpr (j < 2) {
+                    constexpr int K = AX ? 2 : 1;  // AX: aligned pair index -> x-offset
+                    cross[j] = dd1<T, AX>([&](int s) { return a.DIVU(j, K * s); }, c.r);
+                    tauj[j] = dd1<T, AX>([&](int s) { return a.G(j, j, K * s); }, c.r);
+                    hj[j] = dd1<T, AX>([&](int s) { return a.DT(j, j, K * s); }, c.r);
+                }
+            }
+        };
+        axis(std::integral_constant<int, 0>{});
+        axis(std::integral_constant<int, 1>{});
+        axis(std::integral_constant<int, 2>{});
+    } else {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            // optional compiler fence between axes (bounds register use; measured:
+            // the unfenced schedule is 6% faster in DP, neutral elsewhere)
+            if (MPFD_AXIS_FENCE) asm volatile("" ::: "memory");
+            DirVals<T> v;
+            load_dir<T>(a, j, v);
+#pragma unroll
+            for (int phi = 0; phi < 5; ++phi) C[phi][j] = conv_term<T, SPL>(c, v, phi, j);
+            dp[j] = d1v<T>(v.p[0], v.p[1], v.p[3], v.p[4], c.r);
+            pwj[j] = d1v<T>(O::mul(v.p[0], v.u[j][0]), O::mul(v.p[1], v.u[j][1]), O::mul(v.p[3], v.u[j][3]),
+                            O::mul(v.p[4], v.u[j][4]), c.r);
+            if (c.viscous) {
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    lap[i][j] = d2v<T>(v.u[i][0], v.u[i][1], v.u[i][2], v.u[i][3], v.u[i][4], c.r2);
+                if (j < 2) {
+                    cross[j] = d1<T>([&](int s) { return a.DIVU(j, s); }, c.r);
+                    tauj[j] = d1<T>([&](int s) { return a.G(j, j, s); }, c.r);
+                    hj[j] = d1<T>([&](int s) { return a.DT(j, j, s); }, c.r);
+                }
             }
         }
     }
